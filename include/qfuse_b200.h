@@ -1,0 +1,145 @@
+/* qfuse-b200 — C-ABI of the B200-native fused forward + adjoint-gradient
+ * engine for batched state-vector circuits (arXiv 2603.02804).
+ *
+ * This is the drop-in boundary for the reference's hot path. The reference
+ * (qfuse, /root/reference/proj) exposes it as C++ templates; each entry point
+ * below replaces one of them (file:line under proj/):
+ *
+ *   qf_gradient_c64          <- qfuse::gradient<float>          include/qfuse/engine.hpp:139-142
+ *                               qfuse::run_checkpointed<float>  include/qfuse/checkpoint.hpp:65-69
+ *   qf_gradient_pergate_c64  <- qfuse::naive_gradient<float>    include/qfuse/engine.hpp:146-149
+ *                               qfuse::run_checkpointed_naive   include/qfuse/checkpoint.hpp:73-79
+ *   qf_plan_*                <- the same two calls with the circuit planned once and the
+ *                               batch state resident in HBM (a training loop calls
+ *                               gradient() with new theta every step, bench.cpp:114-133)
+ *   qf_last_error            <- the what() of the exception the reference would throw
+ *
+ * Conventions (identical to the reference):
+ *   - states are complex64, interleaved (re, im), sample-major: component (s, x)
+ *     at s*2^(n+1) + 2x (+1)  (statevec.hpp:74-76); qubit t = bit t of x.
+ *   - gates are the flattened IR (fusion.cpp:103-125): rotations u = cos(t/2) I
+ *     - i sin(t/2) P (circuit.cpp:61-73), CZ, CNOT(control=q0, target=q1); every
+ *     parameter slot is used by exactly one rotation (circuit.cpp:52-58).
+ *   - observable: Pauli string masks (x_mask, z_mask) with Y = iXZ
+ *     (circuit.hpp:98-108); y_count is recomputed as popcount(x & z).
+ *   - loss = sum over samples of <psi_s|O|psi_s>; grad[j] = d loss / d theta_j,
+ *     summed over the batch, fp64 (engine.cpp:733-738, :686-689).
+ *
+ * Return codes: 0 ok, 2 invalid argument (std::invalid_argument in the
+ * reference), 3 capacity (qfuse::CapacityError), 4 CUDA/NCCL/internal
+ * (std::logic_error / runtime failures). No exception crosses the ABI.
+ * The caller owns host buffers; the library owns device memory. One context
+ * per device; calls on one context are serialised by the caller.
+ */
+#ifndef QFUSE_B200_H
+#define QFUSE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define QF_OK 0
+#define QF_EINVAL 2
+#define QF_ECAPACITY 3
+#define QF_EDEVICE 4
+
+enum { QF_GATE_ROTATION = 0, QF_GATE_CZ = 1, QF_GATE_CNOT = 2 };
+enum { QF_AXIS_X = 0, QF_AXIS_Y = 1, QF_AXIS_Z = 2 };
+
+/* One flattened gate (qfuse::Gate, circuit.hpp:28-49). 16 bytes. */
+typedef struct qf_gate {
+    uint8_t kind;  /* QF_GATE_* */
+    uint8_t axis;  /* QF_AXIS_* (rotations) */
+    uint16_t pad;
+    uint32_t q0;   /* rotation target, or control */
+    uint32_t q1;   /* target of CZ/CNOT */
+    uint32_t param;/* rotation parameter slot */
+} qf_gate;
+
+/* Mirrors qfuse::RunStats (engine.hpp:54-63) with device-side additions. */
+typedef struct qf_stats {
+    uint64_t forward_passes;     /* fused HBM passes in the forward (incl. replay) */
+    uint64_t backward_passes;    /* fused HBM passes in the backward */
+    uint64_t observable_passes;  /* expectation + adjoint seed passes */
+    uint64_t kernel_launches;    /* kernels launched by this call */
+    uint64_t hbm_bytes;          /* algorithmic HBM bytes moved by the fused passes */
+    uint64_t device_bytes;       /* device memory held by the plan */
+    uint32_t passes_per_layer;   /* P */
+    uint32_t ckpt_layers;        /* k actually used */
+    uint32_t resident;           /* 1 if one sample group stays in shared memory */
+    uint32_t stages;             /* device stages (= layers for HEA) */
+    double device_ms;            /* CUDA-event time of the device work */
+} qf_stats;
+
+typedef struct qf_ctx qf_ctx;
+typedef struct qf_plan qf_plan;
+
+const char *qf_last_error(void);
+const char *qf_version(void);
+
+int qf_ctx_create(int device, qf_ctx **out);
+int qf_ctx_destroy(qf_ctx *ctx);
+/* Optional HBM budget (bytes) checked before allocation; 0 = free memory. */
+int qf_ctx_set_hbm_limit(qf_ctx *ctx, uint64_t bytes);
+
+/* One-shot fused forward + adjoint gradient (the reference's
+ * gradient<float> / run_checkpointed<float>). layers: number of equal
+ * layer periods in the gate list (CheckpointPlan::uniform, checkpoint.cpp:38-49);
+ * ckpt_layers: checkpoint interval k in layers, 0 = engine default; must
+ * divide layers. psi0: host, batch*2^(n+1) floats. grad_out: n_params doubles.
+ * expect_out (nullable): per-sample <O>. stats_out nullable. */
+int qf_gradient_c64(qf_ctx *ctx, const qf_gate *gates, size_t n_gates, uint32_t n_qubits,
+                    uint32_t n_params, uint32_t layers, uint32_t ckpt_layers,
+                    const float *psi0, uint32_t batch, const double *theta,
+                    uint64_t x_mask, uint64_t z_mask, double *loss_out, double *grad_out,
+                    double *expect_out, qf_stats *stats_out);
+
+/* Per-gate (unfused) comparator: one HBM traversal per gate, the
+ * reference's naive_gradient (engine.cpp:856-894). Same arguments. */
+int qf_gradient_pergate_c64(qf_ctx *ctx, const qf_gate *gates, size_t n_gates,
+                            uint32_t n_qubits, uint32_t n_params, uint32_t layers,
+                            uint32_t ckpt_layers, const float *psi0, uint32_t batch,
+                            const double *theta, uint64_t x_mask, uint64_t z_mask,
+                            double *loss_out, double *grad_out, double *expect_out,
+                            qf_stats *stats_out);
+
+/* ---- planned / HBM-resident interface (training loops, bench) ---- */
+
+/* Plans the circuit once (theta-independent) and allocates the batch store,
+ * checkpoint slots and scratch for `batch` samples on ctx's device. */
+int qf_plan_create(qf_ctx *ctx, const qf_gate *gates, size_t n_gates, uint32_t n_qubits,
+                   uint32_t n_params, uint32_t layers, uint32_t ckpt_layers, uint32_t batch,
+                   uint64_t x_mask, uint64_t z_mask, qf_plan **out);
+int qf_plan_destroy(qf_plan *plan);
+/* Batch store input. Host (pageable or pinned) -> device copy. */
+int qf_plan_upload_psi0(qf_plan *plan, const float *psi0_host);
+/* Or point the plan at caller-owned device memory (not copied, not modified). */
+int qf_plan_set_psi0_device(qf_plan *plan, const float *psi0_device);
+/* Fused forward + adjoint gradient. theta/outputs are HOST pointers. */
+int qf_plan_gradient(qf_plan *plan, const double *theta, double *loss_out, double *grad_out,
+                     double *expect_out, qf_stats *stats_out);
+/* Same, device pointers: theta_dev (n_params doubles, device); out_dev receives
+ * [grad (n_params) | loss (1) | expect (batch)] doubles on the device. Enqueued on
+ * the plan's stream; no host synchronisation. */
+int qf_plan_gradient_device(qf_plan *plan, const double *theta_dev, double *out_dev);
+/* Per-gate comparator on the same plan's store. */
+int qf_plan_gradient_pergate(qf_plan *plan, const double *theta, double *loss_out,
+                             double *grad_out, double *expect_out, qf_stats *stats_out);
+/* Forward only: final state (before the observable) to host, complex64. */
+int qf_plan_forward_state(qf_plan *plan, const double *theta, float *psi_out_host);
+/* Stream the plan enqueues on (cudaStream_t as void*) and a sync helper. */
+void *qf_plan_stream(qf_plan *plan);
+int qf_plan_synchronize(qf_plan *plan);
+/* Algorithmic HBM bytes of one fused gradient (schedule of this plan), and
+ * the same split per pass kind, for roofline reporting. */
+int qf_plan_traffic(const qf_plan *plan, uint64_t *total_bytes, uint64_t *pass_bytes,
+                    uint64_t *passes_per_gradient);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* QFUSE_B200_H */

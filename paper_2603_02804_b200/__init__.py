@@ -1,0 +1,9 @@
+"""qfuse-b200: B200-native fused forward + adjoint gradient for batched
+state-vector circuits (arXiv 2603.02804), behind a C-ABI drop-in for the
+reference qfuse engine. See include/qfuse_b200.h and DESIGN.md."""
+from . import circuits
+from .capi import (Context, GradientResult, Plan, QfCapacityError, QfError,
+                   QfInvalidArgument, gradient_c64, load, LIB_PATH, SYMBOLS)
+
+__all__ = ["circuits", "Context", "Plan", "GradientResult", "gradient_c64", "load",
+           "QfError", "QfInvalidArgument", "QfCapacityError", "LIB_PATH", "SYMBOLS"]

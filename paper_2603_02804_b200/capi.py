@@ -1,0 +1,241 @@
+"""ctypes binding of the C-ABI (include/qfuse_b200.h).
+
+The product path is the in-tree ``libqfuse_b200.so`` (CUDA sm_100a). There is
+no CPU fallback: if the library is missing, or no B200 is visible, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+from .circuits import GATE_DTYPE
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libqfuse_b200.so")
+
+QF_OK, QF_EINVAL, QF_ECAPACITY, QF_EDEVICE = 0, 2, 3, 4
+
+# exported symbols, in include/qfuse_b200.h order
+SYMBOLS = (
+    "qf_last_error", "qf_version", "qf_ctx_create", "qf_ctx_destroy", "qf_ctx_set_hbm_limit",
+    "qf_gradient_c64", "qf_gradient_pergate_c64", "qf_plan_create", "qf_plan_destroy",
+    "qf_plan_upload_psi0", "qf_plan_set_psi0_device", "qf_plan_gradient",
+    "qf_plan_gradient_device", "qf_plan_gradient_pergate", "qf_plan_forward_state",
+    "qf_plan_stream", "qf_plan_synchronize", "qf_plan_traffic",
+)
+
+
+class QfError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"qfuse-b200 error {code}: {msg}")
+        self.code = code
+
+
+class QfInvalidArgument(QfError, ValueError):
+    pass
+
+
+class QfCapacityError(QfError, MemoryError):
+    pass
+
+
+class QfStats(C.Structure):
+    _fields_ = [
+        ("forward_passes", C.c_uint64), ("backward_passes", C.c_uint64),
+        ("observable_passes", C.c_uint64), ("kernel_launches", C.c_uint64),
+        ("hbm_bytes", C.c_uint64), ("device_bytes", C.c_uint64),
+        ("passes_per_layer", C.c_uint32), ("ckpt_layers", C.c_uint32),
+        ("resident", C.c_uint32), ("stages", C.c_uint32), ("device_ms", C.c_double),
+    ]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+_P = C.c_void_p
+_lib = None
+
+
+def load(path: str = LIB_PATH):
+    """Load the CUDA library; raises loudly when it is missing (no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise FileNotFoundError(
+            f"{path} not built: run `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(there is no CPU fallback)")
+    L = C.CDLL(path)
+    L.qf_last_error.restype = C.c_char_p
+    L.qf_version.restype = C.c_char_p
+    L.qf_ctx_create.argtypes = [C.c_int, C.POINTER(_P)]
+    L.qf_ctx_destroy.argtypes = [_P]
+    L.qf_ctx_set_hbm_limit.argtypes = [_P, C.c_uint64]
+    grad_args = [_P, _P, C.c_size_t, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, _P,
+                 C.c_uint32, _P, C.c_uint64, C.c_uint64, C.POINTER(C.c_double), _P, _P,
+                 C.POINTER(QfStats)]
+    L.qf_gradient_c64.argtypes = grad_args
+    L.qf_gradient_pergate_c64.argtypes = grad_args
+    L.qf_plan_create.argtypes = [_P, _P, C.c_size_t, C.c_uint32, C.c_uint32, C.c_uint32,
+                                 C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint64, C.POINTER(_P)]
+    L.qf_plan_destroy.argtypes = [_P]
+    L.qf_plan_upload_psi0.argtypes = [_P, _P]
+    L.qf_plan_set_psi0_device.argtypes = [_P, _P]
+    L.qf_plan_gradient.argtypes = [_P, _P, C.POINTER(C.c_double), _P, _P, C.POINTER(QfStats)]
+    L.qf_plan_gradient_pergate.argtypes = L.qf_plan_gradient.argtypes
+    L.qf_plan_gradient_device.argtypes = [_P, _P, _P]
+    L.qf_plan_forward_state.argtypes = [_P, _P, _P]
+    L.qf_plan_stream.argtypes = [_P]
+    L.qf_plan_stream.restype = _P
+    L.qf_plan_synchronize.argtypes = [_P]
+    L.qf_plan_traffic.argtypes = [_P, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64),
+                                  C.POINTER(C.c_uint64)]
+    _lib = L
+    return L
+
+
+def _check(rc: int):
+    if rc == QF_OK:
+        return
+    msg = _lib.qf_last_error().decode()
+    if rc == QF_EINVAL:
+        raise QfInvalidArgument(rc, msg)
+    if rc == QF_ECAPACITY:
+        raise QfCapacityError(rc, msg)
+    raise QfError(rc, msg)
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+def _gates(gates):
+    g = np.ascontiguousarray(gates)
+    if g.dtype != GATE_DTYPE:
+        raise TypeError("gates must use circuits.GATE_DTYPE")
+    return g
+
+
+class Context:
+    def __init__(self, device: int = 0):
+        L = load()
+        h = _P()
+        _check(L.qf_ctx_create(device, C.byref(h)))
+        self.h = h
+        self.device = device
+
+    def set_hbm_limit(self, nbytes: int):
+        _check(_lib.qf_ctx_set_hbm_limit(self.h, nbytes))
+
+    def close(self):
+        if self.h:
+            _lib.qf_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+@dataclass
+class GradientResult:
+    """Mirror of qfuse::GradientResult (engine.hpp:65-69)."""
+    loss: float
+    gradient: np.ndarray
+    expect: np.ndarray
+    stats: dict
+
+
+class Plan:
+    """A planned circuit with its batch store resident in HBM."""
+
+    def __init__(self, ctx: Context, gates, n_qubits: int, n_params: int, layers: int,
+                 ckpt_layers: int, batch: int, pauli):
+        g = _gates(gates)
+        self._gates = g
+        self.ctx = ctx
+        self.n, self.n_params, self.batch = n_qubits, n_params, batch
+        h = _P()
+        _check(_lib.qf_plan_create(ctx.h, _ptr(g), len(g), n_qubits, n_params, layers,
+                                   ckpt_layers, batch, pauli[0], pauli[1], C.byref(h)))
+        self.h = h
+
+    def upload_psi0(self, psi0):
+        a = np.ascontiguousarray(psi0, np.float32)
+        if a.size != self.batch * (2 << self.n):
+            raise ValueError("psi0 shape does not match the plan")
+        _check(_lib.qf_plan_upload_psi0(self.h, _ptr(a)))
+        self.synchronize()
+
+    def upload_psi0_ptr(self, host_ptr: int):
+        _check(_lib.qf_plan_upload_psi0(self.h, C.c_void_p(host_ptr)))
+
+    def set_psi0_device(self, dev_ptr: int):
+        _check(_lib.qf_plan_set_psi0_device(self.h, C.c_void_p(dev_ptr)))
+
+    def gradient(self, theta, pergate: bool = False) -> GradientResult:
+        th = np.ascontiguousarray(theta, np.float64)
+        if th.size != self.n_params:
+            raise QfInvalidArgument(QF_EINVAL, "gradient: theta length mismatch")
+        grad = np.empty(self.n_params, np.float64)
+        exp = np.empty(self.batch, np.float64)
+        loss = C.c_double()
+        st = QfStats()
+        fn = _lib.qf_plan_gradient_pergate if pergate else _lib.qf_plan_gradient
+        _check(fn(self.h, _ptr(th), C.byref(loss), _ptr(grad), _ptr(exp), C.byref(st)))
+        return GradientResult(loss.value, grad, exp, st.as_dict())
+
+    def gradient_device(self, theta_dev_ptr: int, out_dev_ptr: int):
+        _check(_lib.qf_plan_gradient_device(self.h, C.c_void_p(theta_dev_ptr),
+                                            C.c_void_p(out_dev_ptr)))
+
+    def forward_state(self, theta):
+        th = np.ascontiguousarray(theta, np.float64)
+        out = np.empty((self.batch, 1 << self.n, 2), np.float32)
+        _check(_lib.qf_plan_forward_state(self.h, _ptr(th), _ptr(out)))
+        return out
+
+    def stream(self) -> int:
+        return _lib.qf_plan_stream(self.h) or 0
+
+    def synchronize(self):
+        _check(_lib.qf_plan_synchronize(self.h))
+
+    def traffic(self):
+        t, p, n = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        _check(_lib.qf_plan_traffic(self.h, C.byref(t), C.byref(p), C.byref(n)))
+        return t.value, p.value, n.value
+
+    def close(self):
+        if getattr(self, "h", None):
+            _lib.qf_plan_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def gradient_c64(ctx: Context, gates, n_qubits, n_params, layers, ckpt_layers, psi0, theta,
+                 pauli, pergate: bool = False) -> GradientResult:
+    """One-shot qf_gradient_c64 (the reference's gradient<float>/run_checkpointed<float>)."""
+    g = _gates(gates)
+    a = np.ascontiguousarray(psi0, np.float32)
+    batch = a.shape[0]
+    th = np.ascontiguousarray(theta, np.float64)
+    grad = np.empty(n_params, np.float64)
+    exp = np.empty(batch, np.float64)
+    loss = C.c_double()
+    st = QfStats()
+    fn = _lib.qf_gradient_pergate_c64 if pergate else _lib.qf_gradient_c64
+    _check(fn(ctx.h, _ptr(g), len(g), n_qubits, n_params, layers, ckpt_layers, _ptr(a), batch,
+              _ptr(th), pauli[0], pauli[1], C.byref(loss), _ptr(grad), _ptr(exp),
+              C.byref(st)))
+    return GradientResult(loss.value, grad, exp, st.as_dict())

@@ -1,0 +1,701 @@
+// C-ABI of qfuse-b200 (include/qfuse_b200.h): device store, checkpoint
+// slots, the fused schedule and the per-gate comparator.
+//
+// Schedule U: the forward runs every stage's passes in place
+// on one working buffer and lands the last pass of every k-th stage in a
+// checkpoint slot; the backward uncomputes psi with the inverse stages and
+// re-anchors it from the slot at each block end, so the backward never
+// stores an intermediate state (the reference instead replays each block
+// into a ledger, checkpoint.cpp:123-135; both give the same gradients).
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/qfuse_b200.h"
+#include "qf_internal.h"
+#include "qf_plan.h"
+
+using namespace qfb;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct DeviceError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+void ck(cudaError_t e, const char *what) {
+    if (e != cudaSuccess)
+        throw DeviceError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <class F> int guarded(F &&f) {
+    try {
+        f();
+        return QF_OK;
+    } catch (const CapacityError &e) {
+        g_err = e.what();
+        return QF_ECAPACITY;
+    } catch (const std::invalid_argument &e) {
+        g_err = e.what();
+        return QF_EINVAL;
+    } catch (const std::bad_alloc &e) {
+        g_err = "host allocation failed";
+        return QF_ECAPACITY;
+    } catch (const std::exception &e) {
+        g_err = e.what();
+        return QF_EDEVICE;
+    }
+}
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
+                                   const cuuint64_t *, const cuuint64_t *, const cuuint32_t *,
+                                   const cuuint32_t *, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+    });
+    if (!fn) throw DeviceError("cuTensorMapEncodeTiled unavailable");
+    return fn;
+}
+
+CUtensorMap encode(void *base, int rank, const cuuint64_t *dims, const cuuint64_t *strides,
+                   const cuuint32_t *box) {
+    CUtensorMap m;
+    cuuint32_t es[5] = {1, 1, 1, 1, 1};
+    const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rank, base, dims, strides,
+                                   box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw DeviceError("cuTensorMapEncodeTiled failed: " + std::to_string(r));
+    return m;
+}
+
+// 5-D view of a batch store for a streaming pass (see qf_internal.h).
+CUtensorMap pass_map(void *base, const PassLayout &L, uint32_t n, uint32_t batch) {
+    const int a = L.row_start;
+    cuuint64_t dims[5] = {32, 1ull << L.tile_lo_bits, 256, 1ull << L.tile_hi_bits, batch};
+    cuuint64_t strides[4] = {128, 8ull << a, 8ull << (a + 8), 8ull << n};
+    cuuint32_t box[5] = {32, 1, 256, 1, 1};
+    return encode(base, 5, dims, strides, box);
+}
+// 3-D view [buffers][rows][32 floats] for the resident kernel.
+CUtensorMap flat_map(void *base, uint64_t rows, uint64_t nbuf, uint64_t buf_bytes) {
+    cuuint64_t dims[3] = {32, rows, nbuf ? nbuf : 1};
+    cuuint64_t strides[2] = {128, buf_bytes};
+    cuuint32_t box[3] = {32, 256, 1};
+    return encode(base, 3, dims, strides, box);
+}
+
+template <class T> T *dalloc(size_t count, std::vector<void *> &owned) {
+    if (count == 0) count = 1;
+    void *p = nullptr;
+    const cudaError_t e = cudaMalloc(&p, count * sizeof(T));
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        throw CapacityError("device allocation of " + std::to_string(count * sizeof(T)) +
+                            " bytes failed: " + cudaGetErrorString(e));
+    }
+    owned.push_back(p);
+    return static_cast<T *>(p);
+}
+template <class T> T *dupload(const std::vector<T> &v, std::vector<void *> &owned) {
+    T *p = dalloc<T>(v.size(), owned);
+    if (!v.empty()) ck(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice), "upload");
+    return p;
+}
+
+} // namespace
+
+struct qf_ctx {
+    int device = 0;
+    int sms = 148;
+    uint64_t hbm_limit = 0;
+    cudaStream_t stream = nullptr;
+};
+
+struct qf_plan {
+    qf_ctx *ctx = nullptr;
+    Plan P;
+    std::vector<void *> owned;
+    uint64_t amps = 0;        // B * 2^n
+    uint64_t amps_padded = 0; // multiple of one tile
+    size_t state_bytes = 0;
+    // stores
+    float2 *psi0 = nullptr, *W = nullptr, *lam = nullptr, *slots = nullptr, *fout = nullptr;
+    // theta-dependent stage data
+    double *theta = nullptr, *out = nullptr;
+    float2 *ry = nullptr, *tcol = nullptr, *trow = nullptr, *tt1 = nullptr, *tt2 = nullptr;
+    double *wg = nullptr, *wa = nullptr, *wfinal = nullptr, *sec_gamma = nullptr;
+    CzSet *czsets = nullptr;
+    int *stage_cz = nullptr;
+    uint32_t *sec_q = nullptr, *sec_stage = nullptr, *sec_alpha = nullptr, *sec_off = nullptr,
+             *sec_gates = nullptr;
+    double *kpart = nullptr, *kout = nullptr, *epart = nullptr;
+    int grid_fwd = 0, grid_bwd = 0, grid_res = 0;
+    // tensor maps
+    std::vector<CUtensorMap> m_psi0, m_W, m_lam; // per pass
+    std::vector<std::vector<CUtensorMap>> m_slot; // [slot][pass]
+    CUtensorMap r_psi0{}, r_slots{}, r_out{};
+    // per-gate comparator
+    double *gpart = nullptr;
+    uint32_t *rot_params = nullptr;
+    int n_rot = 0, gblocks = 0;
+    // host staging
+    double *h_theta = nullptr, *h_out = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    qf_stats last{};
+
+    ~qf_plan() {
+        if (ctx) cudaSetDevice(ctx->device);
+        for (void *p : owned) cudaFree(p);
+        if (h_theta) cudaFreeHost(h_theta);
+        if (h_out) cudaFreeHost(h_out);
+        if (ev0) cudaEventDestroy(ev0);
+        if (ev1) cudaEventDestroy(ev1);
+    }
+    size_t out_len() const { return size_t(P.n_params) + 1 + P.batch; }
+};
+
+namespace {
+
+void build_device_plan(qf_plan *pl) {
+    const Plan &P = pl->P;
+    qf_ctx *ctx = pl->ctx;
+    ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+    pl->amps = uint64_t(P.batch) << P.n;
+    pl->amps_padded = (pl->amps + kTileAmps - 1) / kTileAmps * kTileAmps;
+    pl->state_bytes = size_t(pl->amps_padded) * 8;
+    const uint32_t S = P.stages, n = P.n;
+
+    // ---- capacity check before touching the allocator (CapacityError as the reference)
+    const int occ_f = pass_occupancy(false), occ_b = pass_occupancy(true), occ_r = resident_occupancy();
+    if (occ_f <= 0 || occ_b <= 0 || occ_r <= 0) throw DeviceError("kernel occupancy query failed");
+    pl->grid_fwd = occ_f * ctx->sms;
+    pl->grid_bwd = occ_b * ctx->sms;
+    const uint64_t tiles_res = pl->amps_padded / kTileAmps;
+    pl->grid_res = int(std::min<uint64_t>(tiles_res, uint64_t(occ_r) * ctx->sms));
+    const int grid_k = P.resident ? pl->grid_res : pl->grid_bwd;
+    const size_t n_states = P.resident ? (2 + P.n_slots) : (3 + P.n_slots);
+    const size_t kpart_bytes = size_t(grid_k) * S * n * 8 * 8;
+    const size_t need = n_states * pl->state_bytes + kpart_bytes + size_t(S) * (784 * 8 + n * 8) +
+                        (size_t(64) << 20);
+    size_t free_b = 0, total_b = 0;
+    ck(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
+    const uint64_t budget = ctx->hbm_limit ? std::min<uint64_t>(ctx->hbm_limit, free_b) : free_b;
+    if (need > budget)
+        throw CapacityError("device working set of " + std::to_string(need >> 20) +
+                            " MiB (states + " + std::to_string(P.n_slots) +
+                            " checkpoint slots) exceeds the HBM budget of " +
+                            std::to_string(budget >> 20) + " MiB");
+
+    auto &o = pl->owned;
+    pl->psi0 = dalloc<float2>(pl->amps_padded, o);
+    ck(cudaMemset(pl->psi0, 0, pl->state_bytes), "memset");
+    pl->lam = dalloc<float2>(pl->amps_padded, o);
+    if (P.resident) {
+        pl->slots = dalloc<float2>(size_t(pl->amps_padded) * std::max<uint32_t>(1, P.n_slots), o);
+        pl->fout = pl->lam; // forward-only output reuses the lambda store
+    } else {
+        pl->W = dalloc<float2>(pl->amps_padded, o);
+        pl->slots = dalloc<float2>(size_t(pl->amps_padded) * std::max<uint32_t>(1, P.n_slots), o);
+    }
+    pl->theta = dalloc<double>(P.n_params, o);
+    pl->out = dalloc<double>(pl->out_len(), o);
+    // stage data; ry defaults to identity, w to zero (entries no section writes)
+    std::vector<float2> ry_init(size_t(std::max<uint32_t>(S, 1)) * n, make_float2(1.f, 0.f));
+    pl->ry = dupload(ry_init, o);
+    pl->wg = dalloc<double>(size_t(S + 1) * n, o);
+    pl->wa = dalloc<double>(size_t(S + 1) * n, o);
+    ck(cudaMemset(pl->wg, 0, size_t(S + 1) * n * 8), "memset");
+    ck(cudaMemset(pl->wa, 0, size_t(S + 1) * n * 8), "memset");
+    pl->wfinal = dalloc<double>(n, o);
+    pl->tcol = dalloc<float2>(size_t(S) * 16, o);
+    pl->trow = dalloc<float2>(size_t(S) * 256, o);
+    pl->tt1 = dalloc<float2>(size_t(S) * 256, o);
+    pl->tt2 = dalloc<float2>(size_t(S) * 256, o);
+    pl->sec_gamma = dalloc<double>(P.sec_q.size(), o);
+    pl->czsets = dupload(P.czsets, o);
+    pl->stage_cz = dupload(P.stage_cz, o);
+    pl->sec_q = dupload(P.sec_q, o);
+    pl->sec_stage = dupload(P.sec_stage, o);
+    pl->sec_alpha = dupload(P.sec_alpha_row, o);
+    pl->sec_off = dupload(P.sec_off, o);
+    pl->sec_gates = dupload(P.sec_gates, o);
+    pl->kpart = dalloc<double>(size_t(grid_k) * S * n * 8, o);
+    pl->kout = dalloc<double>(size_t(S) * n * 8, o);
+    const uint64_t chunks = (1ull << n) >= uint64_t(kTileAmps) ? (1ull << n) / kTileAmps : 1;
+    pl->epart = dalloc<double>(size_t(P.batch) * chunks, o);
+
+    // ---- tensor maps
+    if (P.resident) {
+        const uint64_t rows = pl->amps_padded / 16;
+        pl->r_psi0 = flat_map(pl->psi0, rows, 1, pl->state_bytes);
+        pl->r_slots = flat_map(pl->slots, rows, std::max<uint32_t>(1, P.n_slots), pl->state_bytes);
+        pl->r_out = flat_map(pl->fout, rows, 1, pl->state_bytes);
+    } else {
+        for (const PassLayout &L : P.passes) {
+            pl->m_psi0.push_back(pass_map(pl->psi0, L, n, P.batch));
+            pl->m_W.push_back(pass_map(pl->W, L, n, P.batch));
+            pl->m_lam.push_back(pass_map(pl->lam, L, n, P.batch));
+        }
+        pl->m_slot.resize(P.n_slots);
+        for (uint32_t j = 0; j < P.n_slots; ++j)
+            for (const PassLayout &L : P.passes)
+                pl->m_slot[j].push_back(pass_map(pl->slots + size_t(j) * pl->amps_padded, L, n, P.batch));
+    }
+    // per-gate comparator bookkeeping
+    std::vector<uint32_t> rp;
+    for (const qf_gate &g : P.gates)
+        if (g.kind == QF_GATE_ROTATION) rp.push_back(g.param);
+    pl->n_rot = int(rp.size());
+    pl->rot_params = dupload(rp, o);
+    pl->gblocks = gate_grid(std::max<uint64_t>(1, pl->amps / 2));
+    ck(cudaMallocHost(&pl->h_theta, sizeof(double) * std::max<uint32_t>(1, P.n_params)), "host alloc");
+    ck(cudaMallocHost(&pl->h_out, sizeof(double) * pl->out_len()), "host alloc");
+    ck(cudaEventCreate(&pl->ev0), "event");
+    ck(cudaEventCreate(&pl->ev1), "event");
+    ck(cudaDeviceSynchronize(), "plan setup");
+}
+
+// ---- the fused gradient, enqueued on the context stream
+void enqueue_prep(qf_plan *pl, const double *theta_dev, qf_stats &st) {
+    const Plan &P = pl->P;
+    cudaStream_t s = pl->ctx->stream;
+    ck(launch_prep_sections(s, int(P.sec_q.size()), pl->sec_q, pl->sec_stage, pl->sec_alpha,
+                            pl->sec_off, pl->sec_gates, theta_dev, int(P.n), pl->ry, pl->wg, pl->wa,
+                            pl->sec_gamma),
+       "prep_sections");
+    ck(launch_diag_tables(s, int(P.stages), int(P.n), pl->wg, pl->wa, pl->tcol, pl->trow, pl->tt1,
+                          pl->tt2, pl->wfinal),
+       "diag_tables");
+    st.kernel_launches += 2;
+}
+
+PassParams pass_params(qf_plan *pl, uint32_t stage, int pi, bool bwd, bool write_psi) {
+    const Plan &P = pl->P;
+    const PassLayout &L = P.passes[pi];
+    PassParams p{};
+    p.n = int(P.n);
+    p.stage = int(stage);
+    p.row_start = L.row_start;
+    p.tiles = int(uint64_t(P.batch) << (P.n - 12));
+    p.tile_lo_bits = L.tile_lo_bits;
+    p.tile_hi_bits = L.tile_hi_bits;
+    p.rot_mask = L.rot_mask;
+    p.meas_mask = L.rot_mask;
+    p.has_diag = L.has_diag ? 1 : 0;
+    p.write_psi = write_psi ? 1 : 0;
+    for (int l = 0; l < 12; ++l) p.qmap[l] = L.qmap[l];
+    p.ry = pl->ry + size_t(stage) * P.n;
+    p.tcol = pl->tcol + size_t(stage) * 16;
+    p.trow = pl->trow + size_t(stage) * 256;
+    p.tt1 = pl->tt1 + size_t(stage) * 256;
+    p.tt2 = pl->tt2 + size_t(stage) * 256;
+    p.cz = P.stage_cz[stage] >= 0 ? pl->czsets + P.stage_cz[stage] : nullptr;
+    p.kpart = pl->kpart + size_t(stage) * P.n * 8;
+    p.kstride = (long long)P.stages * P.n * 8;
+    (void)bwd;
+    return p;
+}
+
+void enqueue_fused(qf_plan *pl, const double *theta_dev, double *out_dev, qf_stats &st,
+                   bool forward_only = false) {
+    const Plan &P = pl->P;
+    cudaStream_t s = pl->ctx->stream;
+    const uint32_t S = P.stages, n = P.n;
+    const uint32_t k = P.ckpt_stages;
+    enqueue_prep(pl, theta_dev, st);
+    const double sb = double(pl->amps) * 8.0; // algorithmic bytes of one state
+    double bytes = 0.0;
+    if (P.resident) {
+        if (!forward_only) {
+            ck(cudaMemsetAsync(pl->kpart, 0, size_t(pl->grid_res) * S * n * 8 * 8, s), "memset");
+        }
+        ResidentParams r{};
+        r.n = int(n);
+        r.stages = int(S);
+        r.ckpt = int(k);
+        r.tiles = int(pl->amps_padded / kTileAmps);
+        r.batch = P.batch;
+        r.x_mask = P.x_mask;
+        r.z_mask = P.z_mask;
+        r.y_count = P.y_count;
+        r.ry = pl->ry;
+        r.tcol = pl->tcol;
+        r.trow = pl->trow;
+        r.czsets = pl->czsets;
+        r.stage_cz = pl->stage_cz;
+        r.wfinal = pl->wfinal;
+        r.czfinal = P.final_cz >= 0 ? pl->czsets + P.final_cz : nullptr;
+        r.kpart = pl->kpart;
+        r.expect = out_dev + P.n_params + 1;
+        r.forward_only = forward_only ? 1 : 0;
+        ck(launch_resident(s, pl->grid_res, r, &pl->r_psi0, &pl->r_slots, &pl->r_out), "resident");
+        st.kernel_launches += 1;
+        st.forward_passes = 1;
+        st.backward_passes = forward_only ? 0 : 1;
+        st.observable_passes = forward_only ? 0 : 1;
+        bytes = sb * (1.0 + (forward_only ? 1.0 : 2.0 * P.n_slots));
+        st.passes_per_layer = 1;
+        st.resident = 1;
+    } else {
+        const int NP = int(P.passes.size());
+        // forward
+        for (uint32_t sg = 0; sg < S; ++sg) {
+            for (int pi = 0; pi < NP; ++pi) {
+                const CUtensorMap *in;
+                if (sg == 0 && pi == 0) in = &pl->m_psi0[pi];
+                else if (pi == 0 && sg % k == 0) in = &pl->m_slot[sg / k - 1][pi];
+                else in = &pl->m_W[pi];
+                const bool to_slot = (pi == NP - 1) && ((sg + 1) % k == 0 || sg + 1 == S);
+                const CUtensorMap *outm = to_slot ? &pl->m_slot[sg / k][pi] : &pl->m_W[pi];
+                PassParams p = pass_params(pl, sg, pi, false, true);
+                ck(launch_pass(s, false, std::min(pl->grid_fwd, p.tiles), p, in, outm, nullptr), "pass fwd");
+                st.kernel_launches++;
+                st.forward_passes++;
+                bytes += 2 * sb;
+            }
+        }
+        if (forward_only) {
+            const float2 *fin = S ? pl->slots + size_t(P.n_slots - 1) * pl->amps_padded : pl->psi0;
+            ck(cudaMemcpyAsync(pl->lam, fin, pl->state_bytes, cudaMemcpyDeviceToDevice, s), "copy");
+        } else {
+            // observable step
+            SeedParams sp{};
+            sp.n = int(n);
+            sp.batch = P.batch;
+            sp.x_mask = P.x_mask;
+            sp.z_mask = P.z_mask;
+            sp.y_count = P.y_count;
+            sp.wfinal = pl->wfinal;
+            sp.czfinal = P.final_cz >= 0 ? pl->czsets + P.final_cz : nullptr;
+            sp.psi = S ? pl->slots + size_t(P.n_slots - 1) * pl->amps_padded : pl->psi0;
+            sp.lam = pl->lam;
+            sp.epart = pl->epart;
+            ck(launch_seed(s, sp), "seed");
+            st.kernel_launches++;
+            st.observable_passes++;
+            bytes += 2 * sb;
+            // backward
+            for (int sg = int(S) - 1; sg >= 0; --sg) {
+                for (int pi = NP - 1; pi >= 0; --pi) {
+                    const bool from_slot = (pi == NP - 1) && ((sg + 1) % k == 0 || uint32_t(sg) + 1 == S);
+                    const CUtensorMap *in = from_slot ? &pl->m_slot[sg / k][pi] : &pl->m_W[pi];
+                    const bool write_psi = !(pi == 0 && sg % k == 0);
+                    PassParams p = pass_params(pl, uint32_t(sg), pi, true, write_psi);
+                    ck(launch_pass(s, true, pl->grid_bwd, p, in, &pl->m_W[pi], &pl->m_lam[pi]), "pass bwd");
+                    st.kernel_launches++;
+                    st.backward_passes++;
+                    bytes += (write_psi ? 4 : 3) * sb;
+                }
+            }
+        }
+        st.passes_per_layer = uint32_t(NP);
+        st.resident = 0;
+    }
+    if (!forward_only) {
+        const uint64_t chunks = (1ull << n) >= uint64_t(kTileAmps) ? (1ull << n) / kTileAmps : 1;
+        const int grid_k = P.resident ? pl->grid_res : pl->grid_bwd;
+        ck(launch_reduce(s, (long long)S * n * 8, grid_k, pl->kpart, pl->kout,
+                         P.resident ? nullptr : pl->epart, int(chunks), P.batch,
+                         out_dev + P.n_params + 1),
+           "reduce");
+        ck(launch_finalize(s, int(P.sec_q.size()), pl->sec_q, pl->sec_stage, pl->sec_off,
+                           pl->sec_gates, pl->sec_gamma, theta_dev, int(n), pl->kout, out_dev,
+                           out_dev + P.n_params + 1, P.batch, out_dev + P.n_params),
+           "finalize");
+        st.kernel_launches += 2;
+    }
+    st.hbm_bytes = uint64_t(bytes);
+    st.ckpt_layers = P.ckpt_layers;
+    st.stages = S;
+}
+
+void enqueue_pergate(qf_plan *pl, const double *theta_dev, double *out_dev, qf_stats &st) {
+    const Plan &P = pl->P;
+    cudaStream_t s = pl->ctx->stream;
+    const uint32_t n = P.n;
+    const double sb = double(pl->amps) * 8.0;
+    double bytes = 0;
+    float2 *psi = P.resident ? pl->slots : pl->W;
+    ck(cudaMemcpyAsync(psi, pl->psi0, pl->state_bytes, cudaMemcpyDeviceToDevice, s), "copy");
+    for (const qf_gate &g : P.gates) {
+        ck(launch_gate_fwd(s, psi, int(n), P.batch, g.kind, g.axis, g.q0, g.q1, theta_dev, g.param), "gate fwd");
+        st.kernel_launches++;
+        st.forward_passes++;
+        bytes += 2 * sb;
+    }
+    ck(cudaMemsetAsync(pl->wfinal, 0, n * sizeof(double), s), "memset");
+    SeedParams sp{};
+    sp.n = int(n);
+    sp.batch = P.batch;
+    sp.x_mask = P.x_mask;
+    sp.z_mask = P.z_mask;
+    sp.y_count = P.y_count;
+    sp.wfinal = pl->wfinal;
+    sp.czfinal = nullptr;
+    sp.psi = psi;
+    sp.lam = pl->lam;
+    sp.epart = pl->epart;
+    ck(launch_seed(s, sp), "seed");
+    st.kernel_launches++;
+    st.observable_passes++;
+    bytes += 2 * sb;
+    int r = pl->n_rot;
+    for (size_t i = P.gates.size(); i-- > 0;) {
+        const qf_gate &g = P.gates[i];
+        double *gp = nullptr;
+        if (g.kind == QF_GATE_ROTATION) gp = pl->gpart + size_t(--r) * pl->gblocks;
+        ck(launch_gate_bwd(s, psi, pl->lam, int(n), P.batch, g.kind, g.axis, g.q0, g.q1, theta_dev,
+                           g.param, gp),
+           "gate bwd");
+        st.kernel_launches++;
+        st.backward_passes++;
+        bytes += 4 * sb;
+    }
+    ck(launch_gate_grad_reduce(s, pl->gpart, pl->gblocks, pl->rot_params, pl->n_rot, out_dev), "grad reduce");
+    const uint64_t chunks = (1ull << n) >= uint64_t(kTileAmps) ? (1ull << n) / kTileAmps : 1;
+    ck(launch_reduce(s, 0, 1, nullptr, nullptr, pl->epart, int(chunks), P.batch,
+                     out_dev + P.n_params + 1),
+       "reduce");
+    ck(launch_finalize(s, 0, nullptr, nullptr, nullptr, nullptr, nullptr, theta_dev, int(n), nullptr,
+                       out_dev, out_dev + P.n_params + 1, P.batch, out_dev + P.n_params),
+       "finalize");
+    st.kernel_launches += 3;
+    st.hbm_bytes = uint64_t(bytes);
+    st.passes_per_layer = P.layers ? uint32_t(P.gates.size() / P.layers) : 0;
+}
+
+qf_plan *create_plan(qf_ctx *ctx, const qf_gate *gates, size_t n_gates, uint32_t n, uint32_t n_params,
+                     uint32_t layers, uint32_t ckpt, uint32_t batch, uint64_t x, uint64_t z) {
+    if (!ctx) throw std::invalid_argument("null context");
+    auto pl = std::make_unique<qf_plan>();
+    pl->ctx = ctx;
+    pl->P = make_plan(gates, n_gates, n, n_params, layers, ckpt, batch, x, z);
+    build_device_plan(pl.get());
+    return pl.release();
+}
+
+enum class Mode { Fused, PerGate };
+
+void run_host(qf_plan *pl, const double *theta, double *loss, double *grad, double *expect,
+              qf_stats *stats, Mode mode) {
+    const Plan &P = pl->P;
+    if (P.n_params && !theta) throw std::invalid_argument("gradient: theta length mismatch");
+    if (!loss || (P.n_params && !grad)) throw std::invalid_argument("gradient: null output");
+    ck(cudaSetDevice(pl->ctx->device), "cudaSetDevice");
+    cudaStream_t s = pl->ctx->stream;
+    qf_stats st{};
+    if (P.n_params) std::memcpy(pl->h_theta, theta, sizeof(double) * P.n_params);
+    ck(cudaEventRecord(pl->ev0, s), "event");
+    if (P.n_params)
+        ck(cudaMemcpyAsync(pl->theta, pl->h_theta, sizeof(double) * P.n_params, cudaMemcpyHostToDevice, s), "H2D");
+    if (mode == Mode::Fused) {
+        enqueue_fused(pl, pl->theta, pl->out, st);
+    } else {
+        if (!pl->gpart) pl->gpart = dalloc<double>(size_t(std::max(1, pl->n_rot)) * pl->gblocks, pl->owned);
+        enqueue_pergate(pl, pl->theta, pl->out, st);
+    }
+    ck(cudaMemcpyAsync(pl->h_out, pl->out, sizeof(double) * pl->out_len(), cudaMemcpyDeviceToHost, s), "D2H");
+    ck(cudaEventRecord(pl->ev1, s), "event");
+    ck(cudaStreamSynchronize(s), "gradient");
+    float ms = 0;
+    cudaEventElapsedTime(&ms, pl->ev0, pl->ev1);
+    st.device_ms = ms;
+    st.device_bytes = 0;
+    *loss = pl->h_out[P.n_params];
+    if (P.n_params) std::memcpy(grad, pl->h_out, sizeof(double) * P.n_params);
+    if (expect) std::memcpy(expect, pl->h_out + P.n_params + 1, sizeof(double) * P.batch);
+    pl->last = st;
+    if (stats) *stats = st;
+}
+
+} // namespace
+
+extern "C" {
+
+const char *qf_last_error(void) { return g_err.c_str(); }
+const char *qf_version(void) { return "qfuse-b200 0.1.0 (sm_100a)"; }
+
+int qf_ctx_create(int device, qf_ctx **out) {
+    return guarded([&] {
+        if (!out) throw std::invalid_argument("null output pointer");
+        int count = 0;
+        ck(cudaGetDeviceCount(&count), "cudaGetDeviceCount");
+        if (device < 0 || device >= count) throw std::invalid_argument("no such CUDA device");
+        ck(cudaSetDevice(device), "cudaSetDevice");
+        cudaDeviceProp prop;
+        ck(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+        if (prop.major != 10)
+            throw DeviceError("qfuse-b200 is built for sm_100a (Blackwell B200); device " +
+                              std::string(prop.name) + " is sm_" + std::to_string(prop.major) +
+                              std::to_string(prop.minor));
+        auto c = std::make_unique<qf_ctx>();
+        c->device = device;
+        c->sms = prop.multiProcessorCount;
+        ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream");
+        *out = c.release();
+    });
+}
+
+int qf_ctx_destroy(qf_ctx *ctx) {
+    return guarded([&] {
+        if (!ctx) return;
+        cudaSetDevice(ctx->device);
+        if (ctx->stream) cudaStreamDestroy(ctx->stream);
+        delete ctx;
+    });
+}
+
+int qf_ctx_set_hbm_limit(qf_ctx *ctx, uint64_t bytes) {
+    return guarded([&] {
+        if (!ctx) throw std::invalid_argument("null context");
+        ctx->hbm_limit = bytes;
+    });
+}
+
+int qf_plan_create(qf_ctx *ctx, const qf_gate *gates, size_t n_gates, uint32_t n_qubits,
+                   uint32_t n_params, uint32_t layers, uint32_t ckpt_layers, uint32_t batch,
+                   uint64_t x_mask, uint64_t z_mask, qf_plan **out) {
+    return guarded([&] {
+        if (!out) throw std::invalid_argument("null output pointer");
+        *out = create_plan(ctx, gates, n_gates, n_qubits, n_params, layers, ckpt_layers, batch,
+                           x_mask, z_mask);
+    });
+}
+
+int qf_plan_destroy(qf_plan *plan) {
+    return guarded([&] { delete plan; });
+}
+
+int qf_plan_upload_psi0(qf_plan *plan, const float *psi0_host) {
+    return guarded([&] {
+        if (!plan || !psi0_host) throw std::invalid_argument("null argument");
+        ck(cudaSetDevice(plan->ctx->device), "cudaSetDevice");
+        ck(cudaMemcpyAsync(plan->psi0, psi0_host, plan->amps * 8, cudaMemcpyHostToDevice,
+                           plan->ctx->stream),
+           "H2D psi0");
+    });
+}
+
+int qf_plan_set_psi0_device(qf_plan *plan, const float *psi0_device) {
+    return guarded([&] {
+        if (!plan || !psi0_device) throw std::invalid_argument("null argument");
+        ck(cudaSetDevice(plan->ctx->device), "cudaSetDevice");
+        ck(cudaMemcpyAsync(plan->psi0, psi0_device, plan->amps * 8, cudaMemcpyDeviceToDevice,
+                           plan->ctx->stream),
+           "D2D psi0");
+    });
+}
+
+int qf_plan_gradient(qf_plan *plan, const double *theta, double *loss_out, double *grad_out,
+                     double *expect_out, qf_stats *stats_out) {
+    return guarded([&] {
+        if (!plan) throw std::invalid_argument("null plan");
+        run_host(plan, theta, loss_out, grad_out, expect_out, stats_out, Mode::Fused);
+    });
+}
+
+int qf_plan_gradient_pergate(qf_plan *plan, const double *theta, double *loss_out,
+                             double *grad_out, double *expect_out, qf_stats *stats_out) {
+    return guarded([&] {
+        if (!plan) throw std::invalid_argument("null plan");
+        run_host(plan, theta, loss_out, grad_out, expect_out, stats_out, Mode::PerGate);
+    });
+}
+
+int qf_plan_gradient_device(qf_plan *plan, const double *theta_dev, double *out_dev) {
+    return guarded([&] {
+        if (!plan || !out_dev || (plan->P.n_params && !theta_dev))
+            throw std::invalid_argument("null argument");
+        ck(cudaSetDevice(plan->ctx->device), "cudaSetDevice");
+        qf_stats st{};
+        enqueue_fused(plan, theta_dev, out_dev, st);
+        plan->last = st;
+    });
+}
+
+int qf_plan_forward_state(qf_plan *plan, const double *theta, float *psi_out_host) {
+    return guarded([&] {
+        if (!plan || !psi_out_host) throw std::invalid_argument("null argument");
+        ck(cudaSetDevice(plan->ctx->device), "cudaSetDevice");
+        const Plan &P = plan->P;
+        cudaStream_t s = plan->ctx->stream;
+        if (P.n_params) {
+            std::memcpy(plan->h_theta, theta, sizeof(double) * P.n_params);
+            ck(cudaMemcpyAsync(plan->theta, plan->h_theta, sizeof(double) * P.n_params,
+                               cudaMemcpyHostToDevice, s),
+               "H2D");
+        }
+        qf_stats st{};
+        enqueue_fused(plan, plan->theta, plan->out, st, /*forward_only=*/true);
+        ck(cudaMemcpyAsync(psi_out_host, plan->lam, plan->amps * 8, cudaMemcpyDeviceToHost, s), "D2H");
+        ck(cudaStreamSynchronize(s), "forward");
+    });
+}
+
+void *qf_plan_stream(qf_plan *plan) { return plan ? plan->ctx->stream : nullptr; }
+
+int qf_plan_synchronize(qf_plan *plan) {
+    return guarded([&] {
+        if (!plan) throw std::invalid_argument("null plan");
+        ck(cudaStreamSynchronize(plan->ctx->stream), "synchronize");
+    });
+}
+
+int qf_plan_traffic(const qf_plan *plan, uint64_t *total_bytes, uint64_t *pass_bytes,
+                    uint64_t *passes_per_gradient) {
+    return guarded([&] {
+        if (!plan) throw std::invalid_argument("null plan");
+        const qf_stats &s = plan->last;
+        if (total_bytes) *total_bytes = s.hbm_bytes;
+        if (pass_bytes) *pass_bytes = plan->amps * 8;
+        if (passes_per_gradient) *passes_per_gradient = s.forward_passes + s.backward_passes;
+    });
+}
+
+int qf_gradient_c64(qf_ctx *ctx, const qf_gate *gates, size_t n_gates, uint32_t n_qubits,
+                    uint32_t n_params, uint32_t layers, uint32_t ckpt_layers, const float *psi0,
+                    uint32_t batch, const double *theta, uint64_t x_mask, uint64_t z_mask,
+                    double *loss_out, double *grad_out, double *expect_out, qf_stats *stats_out) {
+    return guarded([&] {
+        if (!psi0) throw std::invalid_argument("null psi0");
+        std::unique_ptr<qf_plan> pl(create_plan(ctx, gates, n_gates, n_qubits, n_params, layers,
+                                                ckpt_layers, batch, x_mask, z_mask));
+        ck(cudaMemcpyAsync(pl->psi0, psi0, pl->amps * 8, cudaMemcpyHostToDevice, ctx->stream), "H2D psi0");
+        run_host(pl.get(), theta, loss_out, grad_out, expect_out, stats_out, Mode::Fused);
+    });
+}
+
+int qf_gradient_pergate_c64(qf_ctx *ctx, const qf_gate *gates, size_t n_gates, uint32_t n_qubits,
+                            uint32_t n_params, uint32_t layers, uint32_t ckpt_layers,
+                            const float *psi0, uint32_t batch, const double *theta,
+                            uint64_t x_mask, uint64_t z_mask, double *loss_out, double *grad_out,
+                            double *expect_out, qf_stats *stats_out) {
+    return guarded([&] {
+        if (!psi0) throw std::invalid_argument("null psi0");
+        std::unique_ptr<qf_plan> pl(create_plan(ctx, gates, n_gates, n_qubits, n_params, layers,
+                                                ckpt_layers, batch, x_mask, z_mask));
+        ck(cudaMemcpyAsync(pl->psi0, psi0, pl->amps * 8, cudaMemcpyHostToDevice, ctx->stream), "H2D psi0");
+        run_host(pl.get(), theta, loss_out, grad_out, expect_out, stats_out, Mode::PerGate);
+    });
+}
+
+} // extern "C"

@@ -1,0 +1,144 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle.
+
+Tolerance (stated by north_star): fp32 gradients within 1e-4
+max-norm relative of the fp64 oracle (rel_diff, acceptance.cpp:63-73); loss
+within 1e-4 * max(|loss_ref|, sum_s |E_s|).
+"""
+import numpy as np
+import pytest
+
+from oracles import rel_diff
+from paper_2603_02804_b200 import circuits as C
+from paper_2603_02804_b200 import capi
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-4
+
+
+def _check(res, oracle_out, tol=TOL):
+    loss, grad, exp = oracle_out
+    assert rel_diff(res.gradient, grad) <= tol, rel_diff(res.gradient, grad)
+    scale = max(abs(loss), float(np.sum(np.abs(exp))), 1e-300)
+    assert abs(res.loss - loss) <= tol * scale, (res.loss, loss)
+    assert rel_diff(res.expect, exp) <= tol, rel_diff(res.expect, exp)
+
+
+def _hea_case(n, layers, batch, label=None, seed=1234):
+    gates, npar = C.build_hea(n, layers)
+    theta = C.random_parameters(npar, seed + 1)
+    psi0 = C.new_random_state(n, batch, seed)
+    pauli = C.parse_pauli(label or C.repeated_ixyz_label(n))
+    return gates, npar, theta, psi0, pauli
+
+
+def test_config1_golden(ctx, oracle):
+    """BASELINE config 1 (4q x 4L, B=8) against the survey's fp64 goldens."""
+    gates, npar, theta, psi0, pauli = _hea_case(4, 4, 8)
+    res = capi.gradient_c64(ctx, gates, 4, npar, 4, 0, psi0, theta, pauli)
+    assert abs(res.loss - (-0.583176427514288)) < 1e-5
+    assert abs(res.gradient.sum() - 3.42181987882572) < 1e-4
+    np.testing.assert_allclose(res.gradient[:4], [-0.280450334533137, -0.847963409542352,
+                                                  0.763083492874858, 0.369861766941313],
+                               atol=1e-5)
+    _check(res, oracle.gradient(gates, 4, npar, psi0, theta, pauli))
+
+
+@pytest.mark.parametrize("label,loss_ref,gsum_ref", [
+    ("ZZZZ", -0.0018511083677094, -2.38131359941164),
+    ("IIIZ", -0.0480468997384506, -1.14539425785954),
+])
+def test_config1_observables(ctx, oracle, label, loss_ref, gsum_ref):
+    gates, npar, theta, psi0, pauli = _hea_case(4, 4, 8, label)
+    res = capi.gradient_c64(ctx, gates, 4, npar, 4, 0, psi0, theta, pauli)
+    assert abs(res.loss - loss_ref) < 1e-5
+    assert abs(res.gradient.sum() - gsum_ref) < 1e-4
+    _check(res, oracle.gradient(gates, 4, npar, psi0, theta, pauli))
+
+
+@pytest.mark.parametrize("n,layers,batch", [
+    (2, 3, 5), (3, 2, 3), (4, 1, 1), (5, 4, 7), (6, 8, 4), (8, 5, 3), (10, 4, 2),
+    (11, 3, 3), (12, 6, 2),          # sample-resident kernel
+    (13, 2, 2), (14, 3, 2), (16, 2, 1),  # streaming passes A + B
+])
+def test_hea_sizes(ctx, oracle, n, layers, batch):
+    gates, npar, theta, psi0, pauli = _hea_case(n, layers, batch, seed=77 + n)
+    res = capi.gradient_c64(ctx, gates, n, npar, layers, 0, psi0, theta, pauli)
+    _check(res, oracle.gradient(gates, n, npar, psi0, theta, pauli))
+
+
+@pytest.mark.parametrize("n,batch", [(20, 1)])
+def test_hea_20q(ctx, oracle, n, batch):
+    gates, npar, theta, psi0, pauli = _hea_case(n, 2, batch, seed=5)
+    res = capi.gradient_c64(ctx, gates, n, npar, 2, 0, psi0, theta, pauli)
+    _check(res, oracle.gradient(gates, n, npar, psi0, theta, pauli))
+
+
+@pytest.mark.parametrize("n,layers", [(6, 8), (14, 4)])
+@pytest.mark.parametrize("k", [1, 2, 4])
+def test_checkpoint_intervals(ctx, oracle, n, layers, k):
+    """run_checkpointed parity: every block size gives the same gradient
+    (checkpoint.cpp:144-163, acceptance C8)."""
+    gates, npar, theta, psi0, pauli = _hea_case(n, layers, 2, seed=13)
+    res = capi.gradient_c64(ctx, gates, n, npar, layers, k, psi0, theta, pauli)
+    _check(res, oracle.gradient(gates, n, npar, psi0, theta, pauli))
+
+
+@pytest.mark.parametrize("n,ngates,seed", [(4, 40, 1), (6, 80, 2), (9, 60, 3), (13, 50, 4)])
+def test_random_circuits(ctx, oracle, n, ngates, seed):
+    """Random Rx/Ry/Rz/CZ/CNOT circuits (test_engine.cpp:438-468)."""
+    gates, npar = C.random_circuit(n, ngates, seed)
+    theta = C.random_parameters(npar, seed + 100)
+    psi0 = C.new_random_state(n, 3, seed + 200)
+    pauli = C.parse_pauli(C.repeated_ixyz_label(n))
+    res = capi.gradient_c64(ctx, gates, n, npar, 0, 0, psi0, theta, pauli)
+    _check(res, oracle.gradient(gates, n, npar, psi0, theta, pauli))
+
+
+@pytest.mark.parametrize("n,layers,batch", [(4, 4, 8), (9, 3, 4), (14, 2, 2)])
+def test_pergate_comparator(ctx, oracle, n, layers, batch):
+    gates, npar, theta, psi0, pauli = _hea_case(n, layers, batch, seed=3)
+    res = capi.gradient_c64(ctx, gates, n, npar, layers, 0, psi0, theta, pauli, pergate=True)
+    _check(res, oracle.gradient(gates, n, npar, psi0, theta, pauli))
+
+
+def test_against_reference_fp32(ctx, ref):
+    """Same inputs through the unmodified reference (gradient<float>)."""
+    n, layers, batch = 8, 6, 4
+    gates, npar, theta, psi0, pauli = _hea_case(n, layers, batch, seed=21)
+    loss_r, grad_r = ref.gradient(gates, n, npar, psi0, theta, pauli, layers=layers)
+    res = capi.gradient_c64(ctx, gates, n, npar, layers, 0, psi0, theta, pauli)
+    assert rel_diff(res.gradient, grad_r) <= TOL
+    assert abs(res.loss - loss_r) <= TOL
+
+
+def test_plan_reuse_and_determinism(ctx, oracle):
+    n, layers, batch = 14, 3, 3
+    gates, npar, theta, psi0, pauli = _hea_case(n, layers, batch, seed=9)
+    plan = capi.Plan(ctx, gates, n, npar, layers, 0, batch, pauli)
+    plan.upload_psi0(psi0)
+    a = plan.gradient(theta)
+    b = plan.gradient(theta)
+    assert np.array_equal(a.gradient, b.gradient) and a.loss == b.loss
+    theta2 = C.random_parameters(npar, 999)
+    c = plan.gradient(theta2)
+    _check(c, oracle.gradient(gates, n, npar, psi0, theta2, pauli))
+
+
+def test_errors(ctx):
+    gates, npar = C.build_hea(4, 2)
+    psi0 = C.new_random_state(4, 2, 1)
+    theta = C.random_parameters(npar, 2)
+    pauli = C.parse_pauli("IXYZ")
+    bad = gates.copy()
+    bad[0]["q0"] = 9
+    with pytest.raises(capi.QfInvalidArgument):
+        capi.gradient_c64(ctx, bad, 4, npar, 2, 0, psi0, theta, pauli)
+    bad = gates.copy()
+    bad[1]["param"] = 0  # parameter used twice
+    with pytest.raises(capi.QfInvalidArgument):
+        capi.gradient_c64(ctx, bad, 4, npar, 2, 0, psi0, theta, pauli)
+    with pytest.raises(capi.QfInvalidArgument):  # k does not divide layers
+        capi.gradient_c64(ctx, gates, 4, npar, 2, 3, psi0, theta, pauli)
+    with pytest.raises(capi.QfCapacityError):
+        g26, np26 = C.build_hea(26, 1)
+        capi.Plan(ctx, g26, 26, np26, 1, 0, 1 << 12, C.parse_pauli("Z" * 26))
