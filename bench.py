@@ -1,0 +1,358 @@
+#!/usr/bin/env python
+"""Benchmark: samples/s of the fused forward + full adjoint gradient of a
+batched 20-qubit HEA (BASELINE.json metric), with HBM roofline, end-to-end
+leg, clocks and the reference's CPU implementation timed on the host.
+
+    python bench.py [--gpus N --steps K --warmup W] [--workload hea20q]
+    python bench.py --impl reference ...      # the reference (oracle/_ref), CPU
+
+Workload (default ``hea20q``): BASELINE config 4's per-GPU shard — HEA 20
+qubits x 1000 layers (60,000 params), 125 samples per GPU, checkpoint every
+10 layers; weak scaling (N GPUs hold N x 125 samples; N = 8 is config 4's
+1000 samples). A step = one fused forward + adjoint gradient over the rank's
+samples plus the NCCL all-reduce of [grad | loss]. Inputs: ψ0 =
+new_random_state<float>(20, N*125, 1234) (each rank its slice of the global
+stream, generated on the device), θ = random_parameters(60000, 1235),
+O = IXYZ.... The state (1 GiB per GPU) is larger than L2.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "samples/sec fwd+adjoint grad, 20q HEA; achieved HBM GB/s vs roofline"
+WORKLOADS = {
+    # name: qubits, layers, per-GPU batch, checkpoint layers, BASELINE config
+    "hea20q": dict(n=20, layers=1000, batch=125, ckpt=10, config="configs[3] per-GPU shard"),
+    "hea16q": dict(n=16, layers=200, batch=1024, ckpt=10, config="configs[2]"),
+    "hea12q": dict(n=12, layers=100, batch=1024, ckpt=10, config="configs[1]"),
+    "hea4q": dict(n=4, layers=4, batch=8, ckpt=0, config="configs[0]"),
+}
+SEED_STATE, SEED_THETA = 1234, 1235
+FALLBACK_HBM_GBS = 6650.0
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.tmp = None
+
+    def start(self):
+        try:
+            self.tmp = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200", "-i", str(self.gpu)], stdout=self.tmp, stderr=subprocess.DEVNULL)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.tmp.flush()
+        rows = []
+        with open(self.tmp.name) as f:
+            for line in f:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) >= 9:
+                    rows.append(parts)
+        os.unlink(self.tmp.name)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = max(float(r[2]) for r in rows if r[2].replace(".", "").isdigit())
+        loaded = [s for s in sm if s > 0.5 * mx] or sm
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i] == "Active"})
+        power = [float(r[3]) for r in rows if r[3].replace(".", "").isdigit()]
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(rows), "power_w_max": max(power) if power else None}
+
+
+# ------------------------------------------------------------ CPU legs
+def reference_sample(ref, n, layers_total, threads, budget_s=12.0):
+    """Time the reference's run_checkpointed<float> (oracle/_ref, OpenMP, all
+    threads) on a bounded sample of the workload and extrapolate linearly in
+    layers (CPU time is linear in B*d)."""
+    import numpy as np
+    from paper_2603_02804_b200 import circuits as C
+    ref.set_threads(threads)
+    batch = max(threads, 1)
+    pauli = C.parse_pauli(C.repeated_ixyz_label(n))
+    # probe one layer to size the sample
+    layers = 1
+    while True:
+        gates, npar = C.build_hea(n, layers)
+        theta = C.random_parameters(npar, SEED_THETA)
+        psi0 = ref.random_state(n, batch, SEED_STATE, np.float32)
+        t0 = time.perf_counter()
+        ref.gradient(gates, n, npar, psi0, theta, pauli, layers=layers, block_layers=1)
+        dt = time.perf_counter() - t0
+        if dt * 2 > budget_s or layers * 2 > layers_total:
+            break
+        layers *= 2
+    sps = batch / dt * (layers / layers_total)
+    sample = (f"{n}q x {layers} layers x {batch} samples (run_checkpointed<float>, k=1) in "
+              f"{dt:.2f} s; samples/s extrapolated x{layers}/{layers_total} to the "
+              f"{layers_total}-layer workload")
+    return sps, sample, (layers, batch, dt)
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracles import RefLib
+    wl = WORKLOADS[args.workload]
+    ref = RefLib()
+    threads = ref.max_threads()
+    vals = []
+    sample = None
+    for i in range(args.warmup + args.steps):
+        v, sample, _ = reference_sample(ref, wl["n"], wl["layers"], threads)
+        if i >= args.warmup:
+            vals.append(v)
+    value = statistics.mean(vals)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "samples/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1000.0 * wl["batch"] * args.gpus / value,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic", "config": workload_config(args, wl),
+        "cpu_baseline": {"value": value, "unit": "samples/s", "cores": threads,
+                         "kind": "reference", "sample": sample},
+        "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def workload_config(args, wl):
+    return {"workload": f"{args.workload}: HEA {wl['n']}q x {wl['layers']}L, "
+                        f"{wl['batch']} samples/GPU ({wl['config']})",
+            "qubits": wl["n"], "layers": wl["layers"], "params": 3 * wl["n"] * wl["layers"],
+            "batch_per_gpu": wl["batch"], "global_batch": wl["batch"] * args.gpus,
+            "ckpt_layers": wl["ckpt"], "observable": "IXYZ repeated",
+            "l2": "inputs larger than L2 (state per GPU > 126 MB)" if wl["n"] >= 16
+            else "state fits L2/smem (sample-resident)",
+            "parallelism": f"dp{args.gpus}"}
+
+
+# ------------------------------------------------------------ GPU arm
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    import paper_2603_02804_b200 as pkg
+    from paper_2603_02804_b200 import circuits as C
+    from paper_2603_02804_b200.parallel import DataParallelGradient
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        log(f"note: WORLD_SIZE={world} but --gpus={args.gpus}; using WORLD_SIZE")
+        args.gpus = world
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    wl = dict(WORKLOADS[args.workload])
+    if args.batch:
+        wl["batch"] = args.batch
+    if args.layers:
+        wl["layers"] = args.layers
+    if args.ckpt is not None:
+        wl["ckpt"] = args.ckpt
+    n, layers, B = wl["n"], wl["layers"], wl["batch"]
+    gates, M = C.build_hea(n, layers)
+    pauli = C.parse_pauli(C.repeated_ixyz_label(n))
+    ctx = pkg.Context(local)
+    plan = pkg.Plan(ctx, gates, n, M, layers, wl["ckpt"], B, pauli)
+    plan.random_psi0(SEED_STATE, first_sample=rank * B)
+    theta_h = torch.from_numpy(C.random_parameters(M, SEED_THETA)).pin_memory()
+    theta_d = theta_h.to("cuda")
+    dp = DataParallelGradient(plan, torch, dist if world > 1 else None)
+    stream = dp.stream
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    # warm-up
+    for _ in range(args.warmup):
+        dp.step_device(theta_d)
+    stream.synchronize()
+    launches_per_step = plan.gradient(theta_h.numpy()).stats["kernel_launches"]
+    plan.set_profiling(True)
+    plan.profile(reset=True)
+
+    sampler = ClockSampler(local) if rank == 0 else None
+    barrier()
+    torch.cuda.synchronize()
+    if sampler:
+        sampler.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        dp.step_device(theta_d)
+    e1.record(stream)
+    stream.synchronize()
+    torch.cuda.synchronize()
+    clocks = sampler.stop() if sampler else None
+    barrier()
+    ms = e0.elapsed_time(e1)
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    prof = plan.profile(reset=True)
+    plan.set_profiling(False)
+    ms_per_step = ms / args.steps
+    value = world * B / (ms_per_step / 1000.0)
+
+    # result sanity (global loss / grad finite)
+    out = dp.out[: M + 1].double().cpu().numpy()
+    assert np.all(np.isfinite(out)), "non-finite gradient"
+
+    # ---- end-to-end leg: host buffers, copies inside the timed region
+    psi_h = torch.empty(B * (2 << n), dtype=torch.float32).pin_memory()
+    plan.download_psi0_ptr(psi_h.data_ptr())
+    res_h = torch.empty(M + 1, dtype=torch.float64).pin_memory()
+    dp.step_host(psi_h, theta_h, theta_d, res_h)
+    stream.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record(stream)
+    for _ in range(args.steps):
+        dp.step_host(psi_h, theta_h, theta_d, res_h)
+    f1.record(stream)
+    stream.synchronize()
+    e2e_ms = f0.elapsed_time(f1)
+    t = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_ms = float(t.item()) / args.steps
+    e2e = {"value": world * B / (e2e_ms / 1000.0), "unit": "samples/s",
+           "h2d_bytes_per_step": int(psi_h.numel() * 4 + theta_h.numel() * 8),
+           "d2h_bytes_per_step": int(res_h.numel() * 8), "ms_per_step": e2e_ms,
+           "api": "capi.Plan.upload_psi0 + qf_plan_gradient_device + NCCL all-reduce + D2H"}
+
+    # ---- roofline of the dominant kernel (backward pass in streaming mode)
+    peak, peak_src = measured_peaks()
+    kinds = {k: v for k, v in prof.items() if v["launches"]}
+    dom = max(kinds, key=lambda k: kinds[k]["ms"])
+    d = kinds[dom]
+    achieved = d["bytes"] / (d["ms"] / 1e3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            traffic = json.load(f).get(f"{args.workload}:{dom}")
+    total_kernel_ms = sum(v["ms"] for v in kinds.values())
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
+                "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                "peak_source": peak_src,
+                "bytes_per_launch": d["bytes"] / d["launches"],
+                "avg_launch_ms": d["ms"] / d["launches"],
+                "share_of_step": d["ms"] / max(total_kernel_ms, 1e-9),
+                "per_kind": {k: {"launches": v["launches"], "ms": v["ms"],
+                                 "GBps": v["bytes"] / (v["ms"] / 1e3) / 1e9 if v["ms"] else None}
+                             for k, v in kinds.items()},
+                "algorithmic_bytes": "per state S = B*2^n*8; fwd pass 2S, bwd pass 4S (3S at a "
+                                     "checkpoint block start), observable 2S"}
+    # whole-step HBM fraction by the BASELINE formula B_U = S(6Pd + d/k + 1)
+    P = 2 if n > 12 else 1
+    k = wl["ckpt"] or min(layers, 10)
+    S = (1 << n) * 8
+    bu = S * (6 * P * layers + layers / k + 1) * B
+    roofline["step_formula_frac"] = bu / (ms_per_step / 1e3) / (peak * 1e9)
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (device SplitMix64/Box-Muller states seed 1234, theta seed 1235)",
+        "config": workload_config(args, wl), "clocks": clocks, "e2e": e2e,
+        "gpu_launches": int(launches_per_step * args.steps), "roofline": roofline,
+    }
+    # ---- CPU baseline: the reference on this host, rank 0 at N = 1 only
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            sys.path.insert(0, os.path.join(ROOT, "tests"))
+            from oracles import RefLib
+            ref = RefLib()
+            th = ref.max_threads()
+            sps, sample, _ = reference_sample(ref, n, layers, th)
+            line["cpu_baseline"] = {"value": sps, "unit": "samples/s", "cores": th,
+                                    "kind": "reference", "sample": sample}
+        except Exception as exc:  # the box may lack the prebuilt reference
+            line["cpu_baseline"] = {"value": None, "unit": "samples/s", "cores": 0,
+                                    "kind": "reference", "sample": f"unavailable: {exc}"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    torch.cuda.synchronize()
+    sys.stdout.flush()
+    sys.stderr.flush()
+    # skip interpreter teardown: torch's allocator must not outlive the plan stream
+    os._exit(0)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="hea20q", choices=sorted(WORKLOADS))
+    ap.add_argument("--batch", type=int, default=0, help="override per-GPU batch")
+    ap.add_argument("--layers", type=int, default=0, help="override layer count")
+    ap.add_argument("--ckpt", type=int, default=None, help="override checkpoint layers")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

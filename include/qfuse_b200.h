@@ -138,6 +138,24 @@ int qf_plan_synchronize(qf_plan *plan);
 int qf_plan_traffic(const qf_plan *plan, uint64_t *total_bytes, uint64_t *pass_bytes,
                     uint64_t *passes_per_gradient);
 
+/* Synthetic batch store on the device: new_random_state<float>(n, batch, seed)
+ * (statevec.cpp:32-53) for samples [first_sample, first_sample + batch) of
+ * the global stream, written straight into the plan's psi0 store. */
+int qf_plan_random_psi0(qf_plan *plan, uint64_t seed, uint64_t first_sample);
+/* Copy the plan's psi0 store back to host memory (batch*2^(n+1) floats). */
+int qf_plan_download_psi0(qf_plan *plan, float *psi0_host);
+
+/* Per-launch CUDA-event profiling by kernel kind (for roofline reporting).
+ * Kinds: 0 forward pass, 1 backward pass, 2 observable, 3 sample-resident,
+ * 4 prep/reduce/finalize, 5 per-gate. bytes = algorithmic HBM bytes. */
+typedef struct qf_profile {
+    uint64_t launches[8];
+    double ms[8];
+    double bytes[8];
+} qf_profile;
+int qf_plan_set_profiling(qf_plan *plan, int enable);
+int qf_plan_profile(qf_plan *plan, qf_profile *out, int reset);
+
 #ifdef __cplusplus
 }
 #endif

@@ -24,8 +24,12 @@ SYMBOLS = (
     "qf_gradient_c64", "qf_gradient_pergate_c64", "qf_plan_create", "qf_plan_destroy",
     "qf_plan_upload_psi0", "qf_plan_set_psi0_device", "qf_plan_gradient",
     "qf_plan_gradient_device", "qf_plan_gradient_pergate", "qf_plan_forward_state",
-    "qf_plan_stream", "qf_plan_synchronize", "qf_plan_traffic",
+    "qf_plan_stream", "qf_plan_synchronize", "qf_plan_traffic", "qf_plan_random_psi0", "qf_plan_download_psi0",
+    "qf_plan_set_profiling", "qf_plan_profile",
 )
+
+PROFILE_KINDS = ("forward_pass", "backward_pass", "observable", "resident", "prep_reduce",
+                 "pergate")
 
 
 class QfError(RuntimeError):
@@ -53,6 +57,10 @@ class QfStats(C.Structure):
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+class QfProfile(C.Structure):
+    _fields_ = [("launches", C.c_uint64 * 8), ("ms", C.c_double * 8), ("bytes", C.c_double * 8)]
 
 
 _P = C.c_void_p
@@ -93,6 +101,10 @@ def load(path: str = LIB_PATH):
     L.qf_plan_synchronize.argtypes = [_P]
     L.qf_plan_traffic.argtypes = [_P, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64),
                                   C.POINTER(C.c_uint64)]
+    L.qf_plan_random_psi0.argtypes = [_P, C.c_uint64, C.c_uint64]
+    L.qf_plan_download_psi0.argtypes = [_P, _P]
+    L.qf_plan_set_profiling.argtypes = [_P, C.c_int]
+    L.qf_plan_profile.argtypes = [_P, C.POINTER(QfProfile), C.c_int]
     _lib = L
     return L
 
@@ -199,6 +211,22 @@ class Plan:
         out = np.empty((self.batch, 1 << self.n, 2), np.float32)
         _check(_lib.qf_plan_forward_state(self.h, _ptr(th), _ptr(out)))
         return out
+
+    def random_psi0(self, seed: int, first_sample: int = 0):
+        """new_random_state<float>(n, batch, seed) generated on the device."""
+        _check(_lib.qf_plan_random_psi0(self.h, seed, first_sample))
+
+    def download_psi0_ptr(self, host_ptr: int):
+        _check(_lib.qf_plan_download_psi0(self.h, C.c_void_p(host_ptr)))
+
+    def set_profiling(self, enable: bool):
+        _check(_lib.qf_plan_set_profiling(self.h, 1 if enable else 0))
+
+    def profile(self, reset: bool = True) -> dict:
+        pr = QfProfile()
+        _check(_lib.qf_plan_profile(self.h, C.byref(pr), 1 if reset else 0))
+        return {k: {"launches": pr.launches[i], "ms": pr.ms[i], "bytes": pr.bytes[i]}
+                for i, k in enumerate(PROFILE_KINDS)}
 
     def stream(self) -> int:
         return _lib.qf_plan_stream(self.h) or 0

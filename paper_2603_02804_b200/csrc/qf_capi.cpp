@@ -138,20 +138,25 @@ struct qf_plan {
     uint64_t amps_padded = 0; // multiple of one tile
     size_t state_bytes = 0;
     // stores
-    float2 *psi0 = nullptr, *W = nullptr, *lam = nullptr, *slots = nullptr, *fout = nullptr;
+    float2 *psi0 = nullptr, *W = nullptr, *lam = nullptr, *slots = nullptr;
     // theta-dependent stage data
     double *theta = nullptr, *out = nullptr;
-    float2 *ry = nullptr, *tcol = nullptr, *trow = nullptr, *tt1 = nullptr, *tt2 = nullptr;
+    float2 *ry = nullptr;
+    DiagTab *dtab = nullptr;
     double *wg = nullptr, *wa = nullptr, *wfinal = nullptr, *sec_gamma = nullptr;
-    CzSet *czsets = nullptr;
-    int *stage_cz = nullptr;
+    // theta-independent tables
+    CzTab *cztab = nullptr;
+    uint32_t *tileinfo = nullptr;
+    std::vector<size_t> tileinfo_off; // [czset * layouts + layout]
+    CzAdj *final_adj = nullptr;
+    int *stage_cz = nullptr, *stage_layout = nullptr, *dq = nullptr;
     uint32_t *sec_q = nullptr, *sec_stage = nullptr, *sec_alpha = nullptr, *sec_off = nullptr,
              *sec_gates = nullptr;
     double *kpart = nullptr, *kout = nullptr, *epart = nullptr;
     int grid_fwd = 0, grid_bwd = 0, grid_res = 0;
     // tensor maps
-    std::vector<CUtensorMap> m_psi0, m_W, m_lam; // per pass
-    std::vector<std::vector<CUtensorMap>> m_slot; // [slot][pass]
+    std::vector<CUtensorMap> m_psi0, m_W, m_lam; // per layout
+    std::vector<std::vector<CUtensorMap>> m_slot; // [slot][layout]
     CUtensorMap r_psi0{}, r_slots{}, r_out{};
     // per-gate comparator
     double *gpart = nullptr;
@@ -161,6 +166,54 @@ struct qf_plan {
     double *h_theta = nullptr, *h_out = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     qf_stats last{};
+    // per-launch CUDA-event profiling (qf_plan_set_profiling)
+    bool profiling = false;
+    std::vector<cudaEvent_t> ev_pool;
+    struct Mark {
+        int kind;
+        size_t e0, e1;
+        double bytes;
+    };
+    std::vector<Mark> marks;
+    size_t ev_used = 0;
+    double prof_ms[8] = {}, prof_bytes[8] = {};
+    uint64_t prof_launches[8] = {};
+    double *rand_scratch = nullptr;
+
+    size_t record() {
+        if (ev_used == ev_pool.size()) {
+            cudaEvent_t e;
+            ck(cudaEventCreate(&e), "event");
+            ev_pool.push_back(e);
+        }
+        ck(cudaEventRecord(ev_pool[ev_used], ctx->stream), "event record");
+        return ev_used++;
+    }
+    // Wraps one launch; kind: 0 fwd pass, 1 bwd pass, 2 observable, 3 resident,
+    // 4 prep/reduce/finalize, 5 per-gate.
+    template <class F> void timed(int kind, double bytes, F &&launch) {
+        if (!profiling) {
+            launch();
+            return;
+        }
+        const size_t a = record();
+        launch();
+        const size_t b = record();
+        marks.push_back({kind, a, b, bytes});
+    }
+    void harvest() {
+        if (marks.empty()) return;
+        ck(cudaStreamSynchronize(ctx->stream), "profile sync");
+        for (const Mark &m : marks) {
+            float ms = 0;
+            ck(cudaEventElapsedTime(&ms, ev_pool[m.e0], ev_pool[m.e1]), "elapsed");
+            prof_ms[m.kind] += ms;
+            prof_bytes[m.kind] += m.bytes;
+            prof_launches[m.kind]++;
+        }
+        marks.clear();
+        ev_used = 0;
+    }
 
     ~qf_plan() {
         if (ctx) cudaSetDevice(ctx->device);
@@ -169,8 +222,12 @@ struct qf_plan {
         if (h_out) cudaFreeHost(h_out);
         if (ev0) cudaEventDestroy(ev0);
         if (ev1) cudaEventDestroy(ev1);
+        for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
     }
     size_t out_len() const { return size_t(P.n_params) + 1 + P.batch; }
+    const uint32_t *tinfo(int cz, int layout) const {
+        return tileinfo + tileinfo_off[size_t(cz) * P.layouts.size() + layout];
+    }
 };
 
 namespace {
@@ -194,7 +251,7 @@ void build_device_plan(qf_plan *pl) {
     const int grid_k = P.resident ? pl->grid_res : pl->grid_bwd;
     const size_t n_states = P.resident ? (2 + P.n_slots) : (3 + P.n_slots);
     const size_t kpart_bytes = size_t(grid_k) * S * n * 8 * 8;
-    const size_t need = n_states * pl->state_bytes + kpart_bytes + size_t(S) * (784 * 8 + n * 8) +
+    const size_t need = n_states * pl->state_bytes + kpart_bytes + size_t(S) * sizeof(DiagTab) +
                         (size_t(64) << 20);
     size_t free_b = 0, total_b = 0;
     ck(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
@@ -209,13 +266,8 @@ void build_device_plan(qf_plan *pl) {
     pl->psi0 = dalloc<float2>(pl->amps_padded, o);
     ck(cudaMemset(pl->psi0, 0, pl->state_bytes), "memset");
     pl->lam = dalloc<float2>(pl->amps_padded, o);
-    if (P.resident) {
-        pl->slots = dalloc<float2>(size_t(pl->amps_padded) * std::max<uint32_t>(1, P.n_slots), o);
-        pl->fout = pl->lam; // forward-only output reuses the lambda store
-    } else {
-        pl->W = dalloc<float2>(pl->amps_padded, o);
-        pl->slots = dalloc<float2>(size_t(pl->amps_padded) * std::max<uint32_t>(1, P.n_slots), o);
-    }
+    if (!P.resident) pl->W = dalloc<float2>(pl->amps_padded, o);
+    pl->slots = dalloc<float2>(size_t(pl->amps_padded) * std::max<uint32_t>(1, P.n_slots), o);
     pl->theta = dalloc<double>(P.n_params, o);
     pl->out = dalloc<double>(pl->out_len(), o);
     // stage data; ry defaults to identity, w to zero (entries no section writes)
@@ -226,13 +278,21 @@ void build_device_plan(qf_plan *pl) {
     ck(cudaMemset(pl->wg, 0, size_t(S + 1) * n * 8), "memset");
     ck(cudaMemset(pl->wa, 0, size_t(S + 1) * n * 8), "memset");
     pl->wfinal = dalloc<double>(n, o);
-    pl->tcol = dalloc<float2>(size_t(S) * 16, o);
-    pl->trow = dalloc<float2>(size_t(S) * 256, o);
-    pl->tt1 = dalloc<float2>(size_t(S) * 256, o);
-    pl->tt2 = dalloc<float2>(size_t(S) * 256, o);
+    pl->dtab = dalloc<DiagTab>(std::max<uint32_t>(S, 1), o);
     pl->sec_gamma = dalloc<double>(P.sec_q.size(), o);
-    pl->czsets = dupload(P.czsets, o);
+    pl->cztab = dupload(P.cztab, o);
+    std::vector<uint32_t> ti_all;
+    for (const auto &t : P.tileinfo) {
+        pl->tileinfo_off.push_back(ti_all.size());
+        ti_all.insert(ti_all.end(), t.begin(), t.end());
+    }
+    pl->tileinfo = dupload(ti_all, o);
+    pl->final_adj = P.final_adj.empty() ? nullptr : dupload(P.final_adj, o);
     pl->stage_cz = dupload(P.stage_cz, o);
+    pl->stage_layout = dupload(P.stage_layout, o);
+    std::vector<int> dq;
+    for (const PassLayout &L : P.layouts) dq.insert(dq.end(), L.dq, L.dq + 28);
+    pl->dq = dupload(dq, o);
     pl->sec_q = dupload(P.sec_q, o);
     pl->sec_stage = dupload(P.sec_stage, o);
     pl->sec_alpha = dupload(P.sec_alpha_row, o);
@@ -248,16 +308,16 @@ void build_device_plan(qf_plan *pl) {
         const uint64_t rows = pl->amps_padded / 16;
         pl->r_psi0 = flat_map(pl->psi0, rows, 1, pl->state_bytes);
         pl->r_slots = flat_map(pl->slots, rows, std::max<uint32_t>(1, P.n_slots), pl->state_bytes);
-        pl->r_out = flat_map(pl->fout, rows, 1, pl->state_bytes);
+        pl->r_out = flat_map(pl->lam, rows, 1, pl->state_bytes);
     } else {
-        for (const PassLayout &L : P.passes) {
+        for (const PassLayout &L : P.layouts) {
             pl->m_psi0.push_back(pass_map(pl->psi0, L, n, P.batch));
             pl->m_W.push_back(pass_map(pl->W, L, n, P.batch));
             pl->m_lam.push_back(pass_map(pl->lam, L, n, P.batch));
         }
         pl->m_slot.resize(P.n_slots);
         for (uint32_t j = 0; j < P.n_slots; ++j)
-            for (const PassLayout &L : P.passes)
+            for (const PassLayout &L : P.layouts)
                 pl->m_slot[j].push_back(pass_map(pl->slots + size_t(j) * pl->amps_padded, L, n, P.batch));
     }
     // per-gate comparator bookkeeping
@@ -278,40 +338,43 @@ void build_device_plan(qf_plan *pl) {
 void enqueue_prep(qf_plan *pl, const double *theta_dev, qf_stats &st) {
     const Plan &P = pl->P;
     cudaStream_t s = pl->ctx->stream;
-    ck(launch_prep_sections(s, int(P.sec_q.size()), pl->sec_q, pl->sec_stage, pl->sec_alpha,
-                            pl->sec_off, pl->sec_gates, theta_dev, int(P.n), pl->ry, pl->wg, pl->wa,
-                            pl->sec_gamma),
-       "prep_sections");
-    ck(launch_diag_tables(s, int(P.stages), int(P.n), pl->wg, pl->wa, pl->tcol, pl->trow, pl->tt1,
-                          pl->tt2, pl->wfinal),
-       "diag_tables");
+    pl->timed(4, 0, [&] {
+        ck(launch_prep_sections(s, int(P.sec_q.size()), pl->sec_q, pl->sec_stage, pl->sec_alpha,
+                                pl->sec_off, pl->sec_gates, theta_dev, int(P.n), pl->ry, pl->wg,
+                                pl->wa, pl->sec_gamma),
+           "prep_sections");
+        ck(launch_diag_tables(s, int(P.stages), int(P.n), pl->wg, pl->wa, pl->stage_layout, pl->dq,
+                              pl->dtab, pl->wfinal),
+           "diag_tables");
+    });
     st.kernel_launches += 2;
 }
 
-PassParams pass_params(qf_plan *pl, uint32_t stage, int pi, bool bwd, bool write_psi) {
+PassParams pass_params(qf_plan *pl, const PassStep &ps, bool write_psi) {
     const Plan &P = pl->P;
-    const PassLayout &L = P.passes[pi];
+    const PassLayout &L = P.layouts[ps.layout];
     PassParams p{};
     p.n = int(P.n);
-    p.stage = int(stage);
-    p.row_start = L.row_start;
     p.tiles = int(uint64_t(P.batch) << (P.n - 12));
     p.tile_lo_bits = L.tile_lo_bits;
     p.tile_hi_bits = L.tile_hi_bits;
     p.rot_mask = L.rot_mask;
-    p.meas_mask = L.rot_mask;
-    p.has_diag = L.has_diag ? 1 : 0;
-    p.write_psi = write_psi ? 1 : 0;
     for (int l = 0; l < 12; ++l) p.qmap[l] = L.qmap[l];
-    p.ry = pl->ry + size_t(stage) * P.n;
-    p.tcol = pl->tcol + size_t(stage) * 16;
-    p.trow = pl->trow + size_t(stage) * 256;
-    p.tt1 = pl->tt1 + size_t(stage) * 256;
-    p.tt2 = pl->tt2 + size_t(stage) * 256;
-    p.cz = P.stage_cz[stage] >= 0 ? pl->czsets + P.stage_cz[stage] : nullptr;
-    p.kpart = pl->kpart + size_t(stage) * P.n * 8;
+    p.s0 = ps.s0;
+    p.s1 = ps.s1;
+    p.nph = ps.nph;
+    for (int i = 0; i < ps.nph; ++i) p.ph[i] = ps.ph[i];
+    p.gd = L.gd;
+    p.ry = pl->ry;
+    if (ps.sd >= 0) {
+        p.dt = pl->dtab + ps.sd;
+        const int c = P.stage_cz[ps.sd];
+        p.cz = c >= 0 ? pl->cztab + size_t(c) * P.layouts.size() + ps.layout : nullptr;
+        p.tileinfo = c >= 0 ? pl->tinfo(c, ps.layout) : nullptr;
+    }
+    p.write_psi = write_psi ? 1 : 0;
+    p.kpart = pl->kpart;
     p.kstride = (long long)P.stages * P.n * 8;
-    (void)bwd;
     return p;
 }
 
@@ -320,107 +383,108 @@ void enqueue_fused(qf_plan *pl, const double *theta_dev, double *out_dev, qf_sta
     const Plan &P = pl->P;
     cudaStream_t s = pl->ctx->stream;
     const uint32_t S = P.stages, n = P.n;
-    const uint32_t k = P.ckpt_stages;
     enqueue_prep(pl, theta_dev, st);
     const double sb = double(pl->amps) * 8.0; // algorithmic bytes of one state
     double bytes = 0.0;
     if (P.resident) {
-        if (!forward_only) {
+        if (!forward_only)
             ck(cudaMemsetAsync(pl->kpart, 0, size_t(pl->grid_res) * S * n * 8 * 8, s), "memset");
-        }
         ResidentParams r{};
         r.n = int(n);
         r.stages = int(S);
-        r.ckpt = int(k);
+        r.ckpt = int(P.ckpt_stages);
         r.tiles = int(pl->amps_padded / kTileAmps);
         r.batch = P.batch;
         r.x_mask = P.x_mask;
         r.z_mask = P.z_mask;
         r.y_count = P.y_count;
         r.ry = pl->ry;
-        r.tcol = pl->tcol;
-        r.trow = pl->trow;
-        r.czsets = pl->czsets;
+        r.dt = pl->dtab;
+        r.cztabs = pl->cztab;
         r.stage_cz = pl->stage_cz;
         r.wfinal = pl->wfinal;
-        r.czfinal = P.final_cz >= 0 ? pl->czsets + P.final_cz : nullptr;
+        r.czfinal = pl->final_adj;
         r.kpart = pl->kpart;
         r.expect = out_dev + P.n_params + 1;
         r.forward_only = forward_only ? 1 : 0;
-        ck(launch_resident(s, pl->grid_res, r, &pl->r_psi0, &pl->r_slots, &pl->r_out), "resident");
+        const double rb = sb * (1.0 + (forward_only ? 1.0 : 2.0 * P.n_slots));
+        pl->timed(3, rb, [&] {
+            ck(launch_resident(s, pl->grid_res, r, &pl->r_psi0, &pl->r_slots, &pl->r_out), "resident");
+        });
         st.kernel_launches += 1;
         st.forward_passes = 1;
         st.backward_passes = forward_only ? 0 : 1;
         st.observable_passes = forward_only ? 0 : 1;
-        bytes = sb * (1.0 + (forward_only ? 1.0 : 2.0 * P.n_slots));
+        bytes = rb;
         st.passes_per_layer = 1;
         st.resident = 1;
     } else {
-        const int NP = int(P.passes.size());
+        const size_t NPS = P.steps.size();
+        const float2 *final_state = NPS ? pl->slots + size_t(P.n_slots - 1) * pl->amps_padded : pl->psi0;
         // forward
-        for (uint32_t sg = 0; sg < S; ++sg) {
-            for (int pi = 0; pi < NP; ++pi) {
-                const CUtensorMap *in;
-                if (sg == 0 && pi == 0) in = &pl->m_psi0[pi];
-                else if (pi == 0 && sg % k == 0) in = &pl->m_slot[sg / k - 1][pi];
-                else in = &pl->m_W[pi];
-                const bool to_slot = (pi == NP - 1) && ((sg + 1) % k == 0 || sg + 1 == S);
-                const CUtensorMap *outm = to_slot ? &pl->m_slot[sg / k][pi] : &pl->m_W[pi];
-                PassParams p = pass_params(pl, sg, pi, false, true);
+        for (size_t pi = 0; pi < NPS; ++pi) {
+            const PassStep &ps = P.steps[pi];
+            const CUtensorMap *in;
+            if (pi == 0) in = &pl->m_psi0[ps.layout];
+            else if (P.slot_pass(pi - 1)) in = &pl->m_slot[(pi - 1) / P.ckpt_passes][ps.layout];
+            else in = &pl->m_W[ps.layout];
+            const CUtensorMap *outm = P.slot_pass(pi) ? &pl->m_slot[pi / P.ckpt_passes][ps.layout] : &pl->m_W[ps.layout];
+            PassParams p = pass_params(pl, ps, true);
+            pl->timed(0, 2 * sb, [&] {
                 ck(launch_pass(s, false, std::min(pl->grid_fwd, p.tiles), p, in, outm, nullptr), "pass fwd");
-                st.kernel_launches++;
-                st.forward_passes++;
-                bytes += 2 * sb;
-            }
-        }
-        if (forward_only) {
-            const float2 *fin = S ? pl->slots + size_t(P.n_slots - 1) * pl->amps_padded : pl->psi0;
-            ck(cudaMemcpyAsync(pl->lam, fin, pl->state_bytes, cudaMemcpyDeviceToDevice, s), "copy");
-        } else {
-            // observable step
-            SeedParams sp{};
-            sp.n = int(n);
-            sp.batch = P.batch;
-            sp.x_mask = P.x_mask;
-            sp.z_mask = P.z_mask;
-            sp.y_count = P.y_count;
-            sp.wfinal = pl->wfinal;
-            sp.czfinal = P.final_cz >= 0 ? pl->czsets + P.final_cz : nullptr;
-            sp.psi = S ? pl->slots + size_t(P.n_slots - 1) * pl->amps_padded : pl->psi0;
-            sp.lam = pl->lam;
-            sp.epart = pl->epart;
-            ck(launch_seed(s, sp), "seed");
+            });
             st.kernel_launches++;
-            st.observable_passes++;
+            st.forward_passes++;
             bytes += 2 * sb;
-            // backward
-            for (int sg = int(S) - 1; sg >= 0; --sg) {
-                for (int pi = NP - 1; pi >= 0; --pi) {
-                    const bool from_slot = (pi == NP - 1) && ((sg + 1) % k == 0 || uint32_t(sg) + 1 == S);
-                    const CUtensorMap *in = from_slot ? &pl->m_slot[sg / k][pi] : &pl->m_W[pi];
-                    const bool write_psi = !(pi == 0 && sg % k == 0);
-                    PassParams p = pass_params(pl, uint32_t(sg), pi, true, write_psi);
-                    ck(launch_pass(s, true, pl->grid_bwd, p, in, &pl->m_W[pi], &pl->m_lam[pi]), "pass bwd");
-                    st.kernel_launches++;
-                    st.backward_passes++;
-                    bytes += (write_psi ? 4 : 3) * sb;
-                }
+        }
+        SeedParams sp{};
+        sp.n = int(n);
+        sp.batch = P.batch;
+        sp.x_mask = P.x_mask;
+        sp.z_mask = P.z_mask;
+        sp.y_count = P.y_count;
+        sp.wfinal = pl->wfinal;
+        sp.czfinal = pl->final_adj;
+        sp.psi = final_state;
+        sp.lam = pl->lam;
+        sp.epart = pl->epart;
+        sp.apply_only = forward_only ? 1 : 0;
+        pl->timed(2, 2 * sb, [&] { ck(launch_seed(s, sp), "seed"); });
+        st.kernel_launches++;
+        st.observable_passes++;
+        bytes += 2 * sb;
+        if (!forward_only) {
+            for (size_t pi = NPS; pi-- > 0;) {
+                const PassStep &ps = P.steps[pi];
+                const bool from_slot = P.slot_pass(pi);
+                const CUtensorMap *in = from_slot ? &pl->m_slot[pi / P.ckpt_passes][ps.layout] : &pl->m_W[ps.layout];
+                const bool write_psi = pi > 0 && !P.slot_pass(pi - 1);
+                PassParams p = pass_params(pl, ps, write_psi);
+                pl->timed(1, (write_psi ? 4 : 3) * sb, [&] {
+                    ck(launch_pass(s, true, pl->grid_bwd, p, in, &pl->m_W[ps.layout], &pl->m_lam[ps.layout]),
+                       "pass bwd");
+                });
+                st.kernel_launches++;
+                st.backward_passes++;
+                bytes += (write_psi ? 4 : 3) * sb;
             }
         }
-        st.passes_per_layer = uint32_t(NP);
+        st.passes_per_layer = S ? uint32_t((NPS + S - 1) / S) : 0;
         st.resident = 0;
     }
     if (!forward_only) {
         const uint64_t chunks = (1ull << n) >= uint64_t(kTileAmps) ? (1ull << n) / kTileAmps : 1;
         const int grid_k = P.resident ? pl->grid_res : pl->grid_bwd;
-        ck(launch_reduce(s, (long long)S * n * 8, grid_k, pl->kpart, pl->kout,
-                         P.resident ? nullptr : pl->epart, int(chunks), P.batch,
-                         out_dev + P.n_params + 1),
-           "reduce");
-        ck(launch_finalize(s, int(P.sec_q.size()), pl->sec_q, pl->sec_stage, pl->sec_off,
-                           pl->sec_gates, pl->sec_gamma, theta_dev, int(n), pl->kout, out_dev,
-                           out_dev + P.n_params + 1, P.batch, out_dev + P.n_params),
-           "finalize");
+        pl->timed(4, 0, [&] {
+            ck(launch_reduce(s, (long long)S * n * 8, grid_k, pl->kpart, pl->kout,
+                             P.resident ? nullptr : pl->epart, int(chunks), P.batch,
+                             out_dev + P.n_params + 1),
+               "reduce");
+            ck(launch_finalize(s, int(P.sec_q.size()), pl->sec_q, pl->sec_stage, pl->sec_off,
+                               pl->sec_gates, pl->sec_gamma, theta_dev, int(n), pl->kout, out_dev,
+                               out_dev + P.n_params + 1, P.batch, out_dev + P.n_params),
+               "finalize");
+        });
         st.kernel_launches += 2;
     }
     st.hbm_bytes = uint64_t(bytes);
@@ -437,7 +501,9 @@ void enqueue_pergate(qf_plan *pl, const double *theta_dev, double *out_dev, qf_s
     float2 *psi = P.resident ? pl->slots : pl->W;
     ck(cudaMemcpyAsync(psi, pl->psi0, pl->state_bytes, cudaMemcpyDeviceToDevice, s), "copy");
     for (const qf_gate &g : P.gates) {
-        ck(launch_gate_fwd(s, psi, int(n), P.batch, g.kind, g.axis, g.q0, g.q1, theta_dev, g.param), "gate fwd");
+        pl->timed(5, 2 * sb, [&] {
+            ck(launch_gate_fwd(s, psi, int(n), P.batch, g.kind, g.axis, g.q0, g.q1, theta_dev, g.param), "gate fwd");
+        });
         st.kernel_launches++;
         st.forward_passes++;
         bytes += 2 * sb;
@@ -451,6 +517,7 @@ void enqueue_pergate(qf_plan *pl, const double *theta_dev, double *out_dev, qf_s
     sp.y_count = P.y_count;
     sp.wfinal = pl->wfinal;
     sp.czfinal = nullptr;
+    sp.apply_only = 0;
     sp.psi = psi;
     sp.lam = pl->lam;
     sp.epart = pl->epart;
@@ -463,9 +530,11 @@ void enqueue_pergate(qf_plan *pl, const double *theta_dev, double *out_dev, qf_s
         const qf_gate &g = P.gates[i];
         double *gp = nullptr;
         if (g.kind == QF_GATE_ROTATION) gp = pl->gpart + size_t(--r) * pl->gblocks;
-        ck(launch_gate_bwd(s, psi, pl->lam, int(n), P.batch, g.kind, g.axis, g.q0, g.q1, theta_dev,
-                           g.param, gp),
-           "gate bwd");
+        pl->timed(5, 4 * sb, [&] {
+            ck(launch_gate_bwd(s, psi, pl->lam, int(n), P.batch, g.kind, g.axis, g.q0, g.q1,
+                               theta_dev, g.param, gp),
+               "gate bwd");
+        });
         st.kernel_launches++;
         st.backward_passes++;
         bytes += 4 * sb;
@@ -699,3 +768,62 @@ int qf_gradient_pergate_c64(qf_ctx *ctx, const qf_gate *gates, size_t n_gates, u
 }
 
 } // extern "C"
+
+extern "C" {
+
+int qf_plan_random_psi0(qf_plan *plan, uint64_t seed, uint64_t first_sample) {
+    return guarded([&] {
+        if (!plan) throw std::invalid_argument("null plan");
+        ck(cudaSetDevice(plan->ctx->device), "cudaSetDevice");
+        const uint64_t dim = 1ull << plan->P.n;
+        const uint64_t chunks = dim >= 4096 ? dim / 4096 : 1;
+        if (!plan->rand_scratch)
+            plan->rand_scratch = dalloc<double>(size_t(plan->P.batch) * chunks, plan->owned);
+        ck(launch_random_state(plan->ctx->stream, seed, first_sample, int(plan->P.n), plan->P.batch,
+                               plan->rand_scratch, plan->psi0),
+           "random psi0");
+        ck(cudaStreamSynchronize(plan->ctx->stream), "random psi0");
+    });
+}
+
+int qf_plan_set_profiling(qf_plan *plan, int enable) {
+    return guarded([&] {
+        if (!plan) throw std::invalid_argument("null plan");
+        plan->profiling = enable != 0;
+    });
+}
+
+int qf_plan_profile(qf_plan *plan, qf_profile *out, int reset) {
+    return guarded([&] {
+        if (!plan) throw std::invalid_argument("null plan");
+        ck(cudaSetDevice(plan->ctx->device), "cudaSetDevice");
+        plan->harvest();
+        if (out) {
+            for (int k = 0; k < 8; ++k) {
+                out->launches[k] = plan->prof_launches[k];
+                out->ms[k] = plan->prof_ms[k];
+                out->bytes[k] = plan->prof_bytes[k];
+            }
+        }
+        if (reset) {
+            for (int k = 0; k < 8; ++k) {
+                plan->prof_launches[k] = 0;
+                plan->prof_ms[k] = 0;
+                plan->prof_bytes[k] = 0;
+            }
+        }
+    });
+}
+
+} // extern "C"
+
+extern "C" int qf_plan_download_psi0(qf_plan *plan, float *psi0_host) {
+    return guarded([&] {
+        if (!plan || !psi0_host) throw std::invalid_argument("null argument");
+        ck(cudaSetDevice(plan->ctx->device), "cudaSetDevice");
+        ck(cudaMemcpyAsync(psi0_host, plan->psi0, plan->amps * 8, cudaMemcpyDeviceToHost,
+                           plan->ctx->stream),
+           "D2H psi0");
+        ck(cudaStreamSynchronize(plan->ctx->stream), "D2H psi0");
+    });
+}

@@ -1,0 +1,338 @@
+// Device building blocks shared by the sm_100a kernels: PTX wrappers for
+// TMA / mbarrier, tile addressing, the Ry / diagonal / K algebra on the
+// 16 register-resident amplitudes of a group phase.
+//
+// Reference semantics restated (paths under /root/reference/proj):
+//   fused forward of a block        engine.cpp:61-109 (composition fusion.cpp:127-152)
+//   CZ parity sign                  engine.cpp:111-136
+//   block backward Re<lam|du|psi>   engine.cpp:265-342
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "qf_internal.h"
+
+namespace qfb {
+namespace dev {
+
+// ------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t su32(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(bar)), "r"(count));
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile("{\n\t.reg .pred p;\n"
+                 "WAIT_%=:\n\t"
+                 "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+                 "@!p bra WAIT_%=;\n}" ::"r"(su32(bar)),
+                 "r"(parity)
+                 : "memory");
+}
+__device__ __forceinline__ void tma_load5(void *dst, const CUtensorMap *map, uint64_t *bar, int c0,
+                                          int c1, int c2, int c3, int c4) {
+    asm volatile("cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes"
+                 " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(su32(dst)),
+                 "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3),
+                 "r"(c4), "r"(su32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void tma_store5(const CUtensorMap *map, const void *src, int c0, int c1,
+                                           int c2, int c3, int c4) {
+    asm volatile("cp.async.bulk.tensor.5d.global.shared::cta.bulk_group"
+                 " [%0, {%1, %2, %3, %4, %5}], [%6];" ::"l"(reinterpret_cast<uint64_t>(map)),
+                 "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(su32(src))
+                 : "memory");
+}
+__device__ __forceinline__ void tma_load3(void *dst, const CUtensorMap *map, uint64_t *bar, int c0,
+                                          int c1, int c2) {
+    asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+                 " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(su32(dst)),
+                 "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(su32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void tma_store3(const CUtensorMap *map, const void *src, int c0, int c1,
+                                           int c2) {
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group"
+                 " [%0, {%1, %2, %3}], [%4];" ::"l"(reinterpret_cast<uint64_t>(map)), "r"(c0),
+                 "r"(c1), "r"(c2), "r"(su32(src))
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;"); }
+__device__ __forceinline__ void bulk_wait_read0() {
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait0() {
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+__device__ __forceinline__ void fence_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void prefetch_map(const CUtensorMap *m) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
+}
+__device__ __forceinline__ uint8_t *align1024(uint8_t *p) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+    return reinterpret_cast<uint8_t *>((a + 1023) & ~uintptr_t(1023));
+}
+
+// ------------------------------------------------------- tile addressing
+// Byte offset of register j of thread tau in group phase G. 16-B chunk c of
+// row r lives at chunk c ^ (r & 7) (SWIZZLE_128B); every phase's LDS/STS
+// pattern is bank-conflict free (G0 as 16-B pairs, G1/G2 as 8-B words).
+template <int G> __device__ __forceinline__ uint32_t goff(uint32_t tau, int j) {
+    if (G == 0) {
+        return (tau << 7) | (((uint32_t(j >> 1) ^ tau) & 7u) << 4) | (uint32_t(j & 1) << 3);
+    } else if (G == 1) {
+        return ((tau >> 4) << 11) | (uint32_t(j) << 7) |
+               (((((tau & 15u) >> 1) ^ uint32_t(j)) & 7u) << 4) | ((tau & 1u) << 3);
+    } else {
+        return (uint32_t(j) << 11) | ((tau >> 4) << 7) |
+               (((((tau & 15u) >> 1) ^ (tau >> 4)) & 7u) << 4) | ((tau & 1u) << 3);
+    }
+}
+__device__ __forceinline__ uint32_t swz(uint32_t l) {
+    const uint32_t r = l >> 4, c = l & 15u;
+    return (r << 7) | ((((c >> 1) ^ r) & 7u) << 4) | ((c & 1u) << 3);
+}
+template <int G>
+__device__ __forceinline__ void lds16(const uint8_t *tile, uint32_t tau, float2 (&v)[16]) {
+    if (G == 0) {
+#pragma unroll
+        for (int j = 0; j < 16; j += 2) {
+            const float4 t = *reinterpret_cast<const float4 *>(tile + goff<0>(tau, j));
+            v[j] = make_float2(t.x, t.y);
+            v[j + 1] = make_float2(t.z, t.w);
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] = *reinterpret_cast<const float2 *>(tile + goff<G>(tau, j));
+    }
+}
+template <int G>
+__device__ __forceinline__ void sts16(uint8_t *tile, uint32_t tau, const float2 (&v)[16]) {
+    if (G == 0) {
+#pragma unroll
+        for (int j = 0; j < 16; j += 2)
+            *reinterpret_cast<float4 *>(tile + goff<0>(tau, j)) =
+                make_float4(v[j].x, v[j].y, v[j + 1].x, v[j + 1].y);
+    } else {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) *reinterpret_cast<float2 *>(tile + goff<G>(tau, j)) = v[j];
+    }
+}
+
+// ------------------------------------------------------ packed complex math
+// Blackwell FFMA2/FMUL2: two fp32 lanes per issue. A complex64 amplitude is
+// one register pair, so real-coefficient updates vectorise over (re, im).
+__device__ __forceinline__ float2 f2mul(float2 a, float2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ float2 f2fma(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+    return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ float2 cmulc(float2 a, float2 b) { // conj(a) * b
+    return make_float2(a.x * b.x + a.y * b.y, a.x * b.y - a.y * b.x);
+}
+
+// Ry(beta) = [[c, -s], [s, c]] (circuit.cpp:67-68) on register bit B;
+// cs = (c, c, s, s). Backward applies Ry(-beta).
+template <int B, bool INV>
+__device__ __forceinline__ void ry2(float2 (&v)[16], float4 cs) {
+    const float2 C = make_float2(cs.x, cs.y);
+    const float2 S = INV ? make_float2(-cs.z, -cs.w) : make_float2(cs.z, cs.w);
+    const float2 N = make_float2(-S.x, -S.y);
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        if (j & (1 << B)) continue;
+        const float2 a = v[j], b = v[j | (1 << B)];
+        v[j] = f2fma(N, b, f2mul(C, a));
+        v[j | (1 << B)] = f2fma(S, a, f2mul(C, b));
+    }
+}
+// One Ry round on the rotated bits of group G (warp-uniform branches).
+template <int G, bool INV>
+__device__ __forceinline__ void ry_round(float2 (&v)[16], const float4 *rys, uint32_t rot) {
+    if (rot & (1u << (4 * G + 0))) ry2<0, INV>(v, rys[4 * G + 0]);
+    if (rot & (1u << (4 * G + 1))) ry2<1, INV>(v, rys[4 * G + 1]);
+    if (rot & (1u << (4 * G + 2))) ry2<2, INV>(v, rys[4 * G + 2]);
+    if (rot & (1u << (4 * G + 3))) ry2<3, INV>(v, rys[4 * G + 3]);
+}
+
+// K_ab = sum psi_a conj(lam_b) over the pairs of register bit B, written as
+// 8 floats (K00, K01, K10, K11 as re, im). With ps = swap(psi):
+// Re = (psi (.) lam).x + .y,  Im = (ps (.) lam).x - .y.
+template <int B>
+__device__ __forceinline__ void kbit(const float2 (&p)[16], const float2 (&ps)[16],
+                                     const float2 (&l)[16], float *k) {
+    float2 a00 = make_float2(0.f, 0.f), b00 = a00, a01 = a00, b01 = a00, a10 = a00, b10 = a00,
+           a11 = a00, b11 = a00;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        if (j & (1 << B)) continue;
+        const int j1 = j | (1 << B);
+        a00 = f2fma(p[j], l[j], a00);
+        b00 = f2fma(ps[j], l[j], b00);
+        a01 = f2fma(p[j], l[j1], a01);
+        b01 = f2fma(ps[j], l[j1], b01);
+        a10 = f2fma(p[j1], l[j], a10);
+        b10 = f2fma(ps[j1], l[j], b10);
+        a11 = f2fma(p[j1], l[j1], a11);
+        b11 = f2fma(ps[j1], l[j1], b11);
+    }
+    k[0] = a00.x + a00.y;
+    k[1] = b00.x - b00.y;
+    k[2] = a01.x + a01.y;
+    k[3] = b01.x - b01.y;
+    k[4] = a10.x + a10.y;
+    k[5] = b10.x - b10.y;
+    k[6] = a11.x + a11.y;
+    k[7] = b11.x - b11.y;
+}
+
+// Reduce-scatter of 32 per-lane values: afterwards lane L holds the warp sum
+// of value L (31 shuffles).
+__device__ __forceinline__ float warp_reduce_scatter32(float (&v)[32]) {
+    const uint32_t lane = threadIdx.x & 31u;
+#pragma unroll
+    for (int m = 16; m >= 1; m >>= 1) {
+        const bool up = (lane & m) != 0;
+#pragma unroll
+        for (int i = 0; i < m; ++i) {
+            const float send = up ? v[i] : v[i + m];
+            const float keep = up ? v[i + m] : v[i];
+            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, m);
+        }
+    }
+    return v[0];
+}
+
+// K of every rotated bit of group G at the current point, added (fp64) to
+// this warp's accumulator acc_w[local bit][8].
+template <int G>
+__device__ __forceinline__ void kmeasure(const float2 (&p)[16], const float2 (&l)[16],
+                                         uint32_t rot, double *acc_w) {
+    if (!(rot & (0xFu << (4 * G)))) return;
+    float2 ps[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) ps[j] = make_float2(p[j].y, p[j].x);
+    float k[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) k[i] = 0.f;
+    if (rot & (1u << (4 * G + 0))) kbit<0>(p, ps, l, k + 0);
+    if (rot & (1u << (4 * G + 1))) kbit<1>(p, ps, l, k + 8);
+    if (rot & (1u << (4 * G + 2))) kbit<2>(p, ps, l, k + 16);
+    if (rot & (1u << (4 * G + 3))) kbit<3>(p, ps, l, k + 24);
+    const float r = warp_reduce_scatter32(k);
+    const uint32_t lane = threadIdx.x & 31u;
+    if (rot & (1u << (4 * G + (lane >> 3)))) acc_w[(4 * G + (lane >> 3)) * 8 + (lane & 7u)] += double(r);
+}
+
+// ------------------------------------------------------------- diagonal
+__device__ __forceinline__ uint32_t linmask4(uint32_t M) {
+    uint32_t m = 0;
+    if (M & 1u) m ^= 0xAAAAu;
+    if (M & 2u) m ^= 0xCCCCu;
+    if (M & 4u) m ^= 0xF0F0u;
+    if (M & 8u) m ^= 0xFF00u;
+    return m;
+}
+struct DiagCtx {
+    float2 base;  // e^{i phi(thread bits, tile bits)}
+    uint32_t sgn; // bit j: sign flip of register j
+};
+// tthr / thrinfo are per-thread constants of a launch; tile terms per tile.
+__device__ __forceinline__ DiagCtx diag_ctx(uint32_t tau, float2 tthr, uint32_t thrinfo,
+                                            const DiagTab *dt, const CzTab *cz,
+                                            const uint32_t *tileinfo, uint32_t tb) {
+    DiagCtx d;
+    float2 b = tthr;
+    if (tb) b = cmul(b, cmul(dt->tt1[tb & 255u], dt->tt2[(tb >> 8) & 255u]));
+    d.base = b;
+    d.sgn = 0;
+    if (cz) {
+        const uint32_t ti = tileinfo ? tileinfo[tb] : 0u;
+        const uint32_t sbase = (ti ^ (thrinfo >> 4) ^ __popc(tau & (ti >> 8))) & 1u;
+        d.sgn = (sbase ? 0xFFFFu : 0u) ^ cz->qreg ^ linmask4(((ti >> 1) ^ thrinfo) & 15u);
+    }
+    return d;
+}
+template <bool CONJ>
+__device__ __forceinline__ void apply_diag(float2 (&v)[16], const DiagCtx &d, const float2 *treg_s) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        float2 g = cmul(d.base, treg_s[j]);
+        const uint32_t flip = (d.sgn << (31 - j)) & 0x80000000u;
+        g.x = __uint_as_float(__float_as_uint(g.x) ^ flip);
+        g.y = __uint_as_float(__float_as_uint(g.y) ^ flip);
+        v[j] = CONJ ? cmulc(g, v[j]) : cmul(g, v[j]);
+    }
+}
+
+// ---------------------------------------------------------- group phases
+struct PhaseEnv {
+    const float4 *rys; // smem [2][12] (c, c, s, s): round 0, round 1
+    uint32_t rot;
+    DiagCtx d;
+    const float2 *treg_s;
+    double *acc_w;     // this warp's [2 rounds][12][8] accumulators
+};
+// ops: 1 = round 0, 2 = diagonal, 4 = round 1.
+template <int G>
+__device__ __forceinline__ void phase_fwd(uint8_t *tile, uint32_t tau, uint32_t ops,
+                                          const PhaseEnv &e) {
+    float2 v[16];
+    lds16<G>(tile, tau, v);
+    if (ops & 1u) ry_round<G, false>(v, e.rys, e.rot);
+    if (ops & 2u) apply_diag<false>(v, e.d, e.treg_s);
+    if (ops & 4u) ry_round<G, false>(v, e.rys + 12, e.rot);
+    sts16<G>(tile, tau, v);
+}
+template <int G>
+__device__ __forceinline__ void phase_bwd(uint8_t *pt, uint8_t *lt, uint32_t tau, uint32_t ops,
+                                          const PhaseEnv &e) {
+    float2 p[16], l[16];
+    lds16<G>(pt, tau, p);
+    lds16<G>(lt, tau, l);
+    if (ops & 4u) {
+        ry_round<G, true>(p, e.rys + 12, e.rot);
+        ry_round<G, true>(l, e.rys + 12, e.rot);
+        kmeasure<G>(p, l, e.rot, e.acc_w + 12 * 8);
+    }
+    if (ops & 2u) {
+        apply_diag<true>(p, e.d, e.treg_s);
+        apply_diag<true>(l, e.d, e.treg_s);
+    }
+    if (ops & 1u) {
+        ry_round<G, true>(p, e.rys, e.rot);
+        ry_round<G, true>(l, e.rys, e.rot);
+        kmeasure<G>(p, l, e.rot, e.acc_w);
+    }
+    sts16<G>(pt, tau, p);
+    sts16<G>(lt, tau, l);
+}
+__device__ __forceinline__ void run_phase_fwd(int g, uint8_t *tile, uint32_t tau, uint32_t ops,
+                                              const PhaseEnv &e) {
+    if (g == 0) phase_fwd<0>(tile, tau, ops, e);
+    else if (g == 1) phase_fwd<1>(tile, tau, ops, e);
+    else phase_fwd<2>(tile, tau, ops, e);
+}
+__device__ __forceinline__ void run_phase_bwd(int g, uint8_t *pt, uint8_t *lt, uint32_t tau,
+                                              uint32_t ops, const PhaseEnv &e) {
+    if (g == 0) phase_bwd<0>(pt, lt, tau, ops, e);
+    else if (g == 1) phase_bwd<1>(pt, lt, tau, ops, e);
+    else phase_bwd<2>(pt, lt, tau, ops, e);
+}
+
+} // namespace dev
+} // namespace qfb

@@ -1,11 +1,10 @@
 // Internal structures shared by the host planner (qf_plan.cpp, qf_capi.cpp)
-// and the sm_100a kernels (qf_kernels.cu). Not part of the C-ABI.
+// and the sm_100a kernels (qf_pass.cu, qf_resident.cu, qf_prep.cu,
+// qf_pergate.cu). Not part of the C-ABI.
 #pragma once
 
 #include <cstddef>
 #include <cstdint>
-#include <string>
-#include <vector>
 
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -14,71 +13,93 @@ namespace qfb {
 
 // ---------------------------------------------------------------- geometry
 // One tile = 4096 amplitudes (32 KiB of complex64) held in shared memory as
-// 256 rows x 16 amplitudes (128 B), TMA SWIZZLE_128B. Local index l (12 bits):
-// bits 0..3 = column = global qubits 0..3; bits 4..11 = row = 8 global qubits
-// (a contiguous block starting at the pass's row_start) or, for n <= 12, the
-// remaining qubits and then sample bits.
+// 256 rows x 16 amplitudes (128 B) with the TMA 128B swizzle. Local index l
+// (12 bits): bits 0..3 = column = global qubits 0..3; bits 4..11 = rows = a
+// contiguous block of 8 qubits starting at the layout's row_start (n > 12),
+// or qubits 4..11 and then sample bits (n <= 12, the sample-resident layout).
+// A thread of a *group phase* G holds local bits [4G, 4G+4) in 16 registers;
+// the other 8 local bits form its thread index tau (in bit order).
 constexpr int kTileBits = 12;
 constexpr int kTileAmps = 1 << kTileBits;
 constexpr int kTileBytes = kTileAmps * 8;
-constexpr int kThreads = 256; // 8 warps; 16 amplitudes per thread per group phase
+constexpr int kThreads = 256;
 constexpr int kMaxQubits = 28;
 
 // Encoded section gate: bits 0..1 kind (0 Rx, 1 Ry, 2 Rz, 3 fixed H), bits 2.. param.
 constexpr uint32_t kSecH = 3u;
 
-// Quadratic-form view of a set of CZ gates (the sign of a diagonal stage):
-// sign(x) = (-1)^{Q(x)}, Q(x) = XOR_{p<q} A_pq x_p x_q.
-struct CzSet {
-    uint32_t adj[32];      // symmetric adjacency (bit p of adj[q] = A_pq)
-    uint32_t adjlo[32];    // adj[q] restricted to bits < q
-    uint32_t qcol;         // 16-bit mask: bit j = Q(j) for the 4 column qubits
+// Diagonal D_s(x) = (-1)^{Q(x)} e^{i sum_q w_q x_q} of one stage, tabulated in
+// the layout of the pass that applies it: register bits of the diag group
+// (treg), the thread bits (tthr), tile bits 0..7 / 8..15 (tt1, tt2).
+struct DiagTab {
+    float2 treg[16];
+    float2 tthr[256];
+    float2 tt1[256];
+    float2 tt2[256];
+};
+
+// A CZ set (quadratic form Q) in one layout/diag group (theta-independent).
+// sign bit of register j for thread tau in tile tb:
+//   sbase = Q(tile) ^ Q(thr) ^ parity(tau & Rtile), M = Mtile ^ Mthr,
+//   sgn   = (sbase ? 0xFFFF : 0) ^ qreg ^ linmask(M)
+// thrinfo[tau] = Q(thr) << 4 | Mthr;  tileinfo[tb] = Q(tile) | Mtile << 1 | Rtile << 8.
+struct CzTab {
+    uint32_t qreg;
     uint32_t pad[3];
-    uint8_t rowinfo[256];  // pass-A rows: bit 4 = Q(r<<4), bits 0..3 = col mask of A*(r<<4)
+    uint16_t thrinfo[256];
 };
 
-// Per-launch parameters of a streaming pass (forward or backward).
+// Adjacency of a CZ set, for the observable fold (seed).
+struct CzAdj {
+    uint32_t adjlo[32]; // bit p < q of adjlo[q] = CZ(p, q)
+};
+
+// One fused HBM pass over the batch store. It applies, in shared memory, up
+// to two Ry rounds on its resident qubits with the stage diagonal between
+// them:  Ry_{s0}(X) -> D -> Ry_{s1}(X)  (forward), or the inverse with K
+// accumulation (backward). ops per phase: bit 0 = round 0, 1 = diag, 2 = round 1.
+struct PassPhase {
+    int8_t g;
+    uint8_t ops;
+};
 struct PassParams {
-    int n;             // qubits
-    int stage;         // device stage (layer)
-    int row_start;     // first global qubit of the 8 row bits (4 for pass A)
-    int tiles;         // tiles in the launch
+    int n;
+    int tiles;
     int tile_lo_bits;  // tile bits between the column and the rows (row_start - 4)
-    int tile_hi_bits;  // tile bits above the rows within a sample (n - row_start - 8)
-    uint32_t rot_mask; // 12 local bits that carry an Ry this pass
-    uint32_t meas_mask;// local bits whose K is accumulated (backward)
-    int has_diag;      // pass A: stage diagonal D_s applied (fwd: first; bwd: last)
-    int write_psi;     // backward: store psi (0 at a checkpoint block start)
-    int qmap[12];      // local bit -> global qubit
-    const float2 *ry;  // [n] (cos, sin) of beta/2 for this stage
-    const float2 *tcol;// [16] diag table of this stage (column bits)
-    const float2 *trow;// [256]
-    const float2 *tt1; // [256] tile bits 12..19
-    const float2 *tt2; // [256] tile bits 20..27
-    const CzSet *cz;   // CZ set of this stage's diagonal (nullptr = none)
-    double *kpart;     // backward: &kpart[0][stage][0][0], layout [grid][stages][n][8]
-    long long kstride; // stages*n*8: distance between CTAs in kpart
+    int tile_hi_bits;  // tile bits above the rows (n - row_start - 8)
+    uint32_t rot_mask; // local bits rotated by this layout
+    int qmap[12];      // local bit -> qubit
+    int s0, s1;        // stages of rounds 0 / 1 (-1 = absent)
+    int nph;
+    PassPhase ph[6];
+    int gd;            // group phase that applies the diagonal
+    const float2 *ry;  // [stages][n] (cos, sin) of beta/2
+    const DiagTab *dt; // diagonal of this pass (nullptr = none)
+    const CzTab *cz;   // its CZ set in this layout (nullptr = none)
+    const uint32_t *tileinfo;
+    int write_psi;     // backward: store psi (0 when the next reader is a slot)
+    double *kpart;     // backward: [grid][stages][n][8]
+    long long kstride; // stages*n*8
 };
 
-// Parameters of the sample-resident kernel (n <= 12): the whole circuit runs
-// on one tile of packed samples held in shared memory.
+// n <= 12: a tile holds 2^(12-n) whole samples; every stage runs in smem.
 struct ResidentParams {
     int n;
     int stages;
-    int ckpt;          // checkpoint interval in stages (re-anchor the uncompute)
+    int ckpt; // re-anchor the uncompute every ckpt stages
     int tiles;
     uint32_t batch;
     uint64_t x_mask, z_mask;
     uint32_t y_count;
-    const float2 *ry;  // [stages][n]
-    const float2 *tcol, *trow; // [stages][16], [stages][256]
-    const CzSet *czsets;       // distinct CZ sets
-    const int *stage_cz;       // [stages] index into czsets or -1
+    const float2 *ry;          // [stages][n]
+    const DiagTab *dt;         // [stages]
+    const CzTab *cztabs;       // distinct CZ sets in the resident layout
+    const int *stage_cz;       // [stages] -> cztabs index or -1
     const double *wfinal;      // [n] final diagonal phases
-    const CzSet *czfinal;      // final CZ set (nullptr = none)
-    double *kpart;             // [stages][n][8][grid]
+    const CzAdj *czfinal;      // nullptr = none
+    double *kpart;             // [grid][stages][n][8]
     double *expect;            // [batch]
-    int forward_only;          // 1: forward then store the final state
+    int forward_only;          // forward, fold D_f, store the final state
 };
 
 struct SeedParams {
@@ -87,21 +108,23 @@ struct SeedParams {
     uint64_t x_mask, z_mask;
     uint32_t y_count;
     const double *wfinal;
-    const CzSet *czfinal;
+    const CzAdj *czfinal;
     const float2 *psi;
     float2 *lam;
-    double *epart; // [batch][chunks]
+    double *epart;  // [batch][chunks]
+    int apply_only; // 1: lam = D_f psi (forward-state readout), no observable
 };
 
-// Kernel launchers (qf_kernels.cu).
+// ------------------------------------------------------------- launchers
 cudaError_t launch_prep_sections(cudaStream_t st, int n_sec, const uint32_t *sec_q,
                                  const uint32_t *sec_stage, const uint32_t *sec_alpha_row,
                                  const uint32_t *sec_off, const uint32_t *sec_gates,
                                  const double *theta, int n, float2 *ry, double *wg,
                                  double *wa, double *sec_gamma);
+// dq: [layouts][28] qubit of (reg 0..3, thr 0..7, tile 0..15), -1 = none.
 cudaError_t launch_diag_tables(cudaStream_t st, int stages, int n, const double *wg,
-                               const double *wa, float2 *tcol, float2 *trow, float2 *tt1,
-                               float2 *tt2, double *wfinal);
+                               const double *wa, const int *stage_layout, const int *dq,
+                               DiagTab *dt, double *wfinal);
 cudaError_t launch_pass(cudaStream_t st, bool backward, int grid, const PassParams &p,
                         const CUtensorMap *psi_in, const CUtensorMap *psi_out,
                         const CUtensorMap *lam);
@@ -117,6 +140,8 @@ cudaError_t launch_finalize(cudaStream_t st, int n_sec, const uint32_t *sec_q,
                             const uint32_t *sec_gates, const double *sec_gamma,
                             const double *theta, int n, const double *kout, double *grad,
                             const double *expect, uint32_t batch, double *loss);
+cudaError_t launch_random_state(cudaStream_t st, uint64_t seed, uint64_t first_sample, int n,
+                                uint32_t batch, double *scratch, float2 *out);
 int pass_occupancy(bool backward);
 int resident_occupancy();
 size_t pass_smem_bytes(bool backward);

@@ -1,0 +1,177 @@
+// Streaming fused pass (n > 12): one HBM round trip of the batch store per
+// pass. Persistent CTAs walk the tiles of the pass layout; each tile is
+// loaded by TMA (SWIZZLE_128B) into shared memory, transformed by 1-5 group
+// phases (registers + FFMA2), and stored back by TMA while the next tile's
+// load is already in flight (double buffer, mbarrier completion).
+//
+// A pass applies  Ry_{s0}(X) -> D -> Ry_{s1}(X)  on its resident qubits X,
+// so with two alternating layouts (qubits 0..11 / 0..3 + top 8) every stage
+// costs ONE pass (the diagonal commutes with everything but the Ry's of its
+// own stage boundary). Backward passes undo the same ops on psi and lambda
+// and accumulate K = sum psi lambda^dag per (stage, qubit) in fp64.
+#include "qf_device.cuh"
+
+namespace qfb {
+namespace {
+
+using namespace dev;
+
+constexpr size_t kAccBytes = size_t(8) * 2 * 12 * 8 * sizeof(double); // [warp][round][bit][8]
+
+constexpr size_t pass_smem(bool bwd) {
+    return size_t(2) * kTileBytes * (bwd ? 2 : 1) + 64 /*mbar*/ + 24 * 16 /*rys*/ +
+           16 * 8 /*treg*/ + (bwd ? kAccBytes : 0) + 1024 /*align*/;
+}
+
+template <bool BWD>
+__global__ void __launch_bounds__(kThreads, BWD ? 1 : 2)
+    pass_kernel(const __grid_constant__ PassParams p, const __grid_constant__ CUtensorMap m_in,
+                const __grid_constant__ CUtensorMap m_out,
+                const __grid_constant__ CUtensorMap m_lam) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = align1024(smem_raw);
+    constexpr uint32_t kBuf = uint32_t(kTileBytes) * (BWD ? 2 : 1);
+    uint8_t *buf[2] = {smem, smem + kBuf};
+    uint8_t *tail = smem + 2 * kBuf;
+    uint64_t *mbar = reinterpret_cast<uint64_t *>(tail);
+    float4 *rys = reinterpret_cast<float4 *>(tail + 64);
+    float2 *treg_s = reinterpret_cast<float2 *>(tail + 64 + 24 * 16);
+    double *acc = reinterpret_cast<double *>(tail + 64 + 24 * 16 + 16 * 8);
+    const uint32_t tid = threadIdx.x, warp = tid >> 5;
+
+    if (tid < 24) {
+        const int r = tid / 12, lb = tid % 12;
+        const int s = r == 0 ? p.s0 : p.s1;
+        float4 v = make_float4(1.f, 1.f, 0.f, 0.f);
+        if (s >= 0 && ((p.rot_mask >> lb) & 1u)) {
+            const float2 cs = p.ry[size_t(s) * p.n + p.qmap[lb]];
+            v = make_float4(cs.x, cs.x, cs.y, cs.y);
+        }
+        rys[tid] = v;
+    } else if (tid < 40) {
+        treg_s[tid - 24] = p.dt ? p.dt->treg[tid - 24] : make_float2(1.f, 0.f);
+    }
+    if (BWD) {
+        for (uint32_t i = tid; i < kAccBytes / 8; i += kThreads) acc[i] = 0.0;
+    }
+    const float2 tthr = p.dt ? p.dt->tthr[tid] : make_float2(1.f, 0.f);
+    const uint32_t thrinfo = p.cz ? p.cz->thrinfo[tid] : 0u;
+    if (tid == 0) {
+        prefetch_map(&m_in);
+        prefetch_map(&m_out);
+        if (BWD) prefetch_map(&m_lam);
+        mbar_init(&mbar[0], 1);
+        mbar_init(&mbar[1], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    const int lo_mask = (1 << p.tile_lo_bits) - 1, hi_mask = (1 << p.tile_hi_bits) - 1;
+    const int sample_shift = p.tile_lo_bits + p.tile_hi_bits;
+    const uint32_t tis_mask = (1u << sample_shift) - 1u;
+    auto issue_load = [&](int t, int b) {
+        const int c1 = t & lo_mask, c3 = (t >> p.tile_lo_bits) & hi_mask, c4 = t >> sample_shift;
+        mbar_expect_tx(&mbar[b], kBuf);
+        tma_load5(buf[b], &m_in, &mbar[b], 0, c1, 0, c3, c4);
+        if (BWD) tma_load5(buf[b] + kTileBytes, &m_lam, &mbar[b], 0, c1, 0, c3, c4);
+    };
+    const int stride = gridDim.x;
+    if (tid == 0) {
+        if (int(blockIdx.x) < p.tiles) issue_load(blockIdx.x, 0);
+        if (int(blockIdx.x) + stride < p.tiles) issue_load(blockIdx.x + stride, 1);
+    }
+    PhaseEnv env;
+    env.rys = rys;
+    env.rot = p.rot_mask;
+    env.treg_s = treg_s;
+    env.acc_w = acc + warp * 2 * 12 * 8;
+    env.d.base = make_float2(1.f, 0.f);
+    env.d.sgn = 0;
+    int it = 0;
+    for (int t = blockIdx.x; t < p.tiles; t += stride, ++it) {
+        const int b = it & 1;
+        if (p.dt) env.d = diag_ctx(tid, tthr, thrinfo, p.dt, p.cz, p.tileinfo, uint32_t(t) & tis_mask);
+        mbar_wait(&mbar[b], (it >> 1) & 1);
+        uint8_t *pt = buf[b];
+        if (!BWD) {
+            for (int i = 0; i < p.nph; ++i) {
+                if (i) __syncthreads();
+                run_phase_fwd(p.ph[i].g, pt, tid, p.ph[i].ops, env);
+            }
+        } else {
+            for (int i = p.nph - 1; i >= 0; --i) {
+                if (i != p.nph - 1) __syncthreads();
+                run_phase_bwd(p.ph[i].g, pt, pt + kTileBytes, tid, p.ph[i].ops, env);
+            }
+        }
+        fence_async_smem();
+        __syncthreads();
+        if (tid == 0) {
+            const int c1 = t & lo_mask, c3 = (t >> p.tile_lo_bits) & hi_mask, c4 = t >> sample_shift;
+            if (!BWD || p.write_psi) tma_store5(&m_out, pt, 0, c1, 0, c3, c4);
+            if (BWD) tma_store5(&m_lam, pt + kTileBytes, 0, c1, 0, c3, c4);
+            bulk_commit();
+            const int tn = t + 2 * stride;
+            if (tn < p.tiles) {
+                bulk_wait_read0();
+                issue_load(tn, b);
+            }
+        }
+    }
+    if (tid == 0) bulk_wait0();
+    if (BWD) {
+        __syncthreads();
+        if (tid < 2 * 12 * 8) {
+            const int r = tid / 96, lb = (tid / 8) % 12, c = tid & 7;
+            const int s = r == 0 ? p.s0 : p.s1;
+            if (s >= 0 && ((p.rot_mask >> lb) & 1u)) {
+                double sum = 0.0;
+#pragma unroll
+                for (int w = 0; w < 8; ++w) sum += acc[((w * 2 + r) * 12 + lb) * 8 + c];
+                p.kpart[size_t(blockIdx.x) * size_t(p.kstride) + size_t(s) * p.n * 8 +
+                        size_t(p.qmap[lb]) * 8 + c] = sum;
+            }
+        }
+    }
+}
+
+bool g_attrs = false;
+cudaError_t ensure_attrs() {
+    if (g_attrs) return cudaSuccess;
+    cudaError_t e = cudaFuncSetAttribute(pass_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(pass_smem(false)));
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(pass_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(pass_smem(true)));
+    g_attrs = e == cudaSuccess;
+    return e;
+}
+
+} // namespace
+
+size_t pass_smem_bytes(bool backward) { return pass_smem(backward); }
+
+int pass_occupancy(bool backward) {
+    if (ensure_attrs() != cudaSuccess) return 0;
+    int blocks = 0;
+    if (backward)
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, pass_kernel<true>, kThreads, pass_smem(true));
+    else
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, pass_kernel<false>, kThreads, pass_smem(false));
+    return blocks;
+}
+
+cudaError_t launch_pass(cudaStream_t st, bool backward, int grid, const PassParams &p,
+                        const CUtensorMap *psi_in, const CUtensorMap *psi_out,
+                        const CUtensorMap *lam) {
+    cudaError_t e = ensure_attrs();
+    if (e != cudaSuccess) return e;
+    const CUtensorMap &l = lam ? *lam : *psi_out;
+    if (backward)
+        pass_kernel<true><<<grid, kThreads, pass_smem(true), st>>>(p, *psi_in, *psi_out, l);
+    else
+        pass_kernel<false><<<grid, kThreads, pass_smem(false), st>>>(p, *psi_in, *psi_out, l);
+    return cudaGetLastError();
+}
+
+} // namespace qfb

@@ -21,31 +21,6 @@
 
 namespace qfb {
 
-CzSet make_czset(const std::vector<std::pair<uint32_t, uint32_t>> &pairs) {
-    CzSet c{};
-    for (auto [a, b] : pairs) { // repeated CZ pairs cancel (parity)
-        c.adj[a] ^= 1u << b;
-        c.adj[b] ^= 1u << a;
-    }
-    for (int q = 0; q < 32; ++q) c.adjlo[q] = c.adj[q] & ((1u << q) - 1u);
-    auto qform = [&](uint32_t v) {
-        uint32_t par = 0;
-        for (int q = 0; q < 32; ++q)
-            if ((v >> q) & 1u) par ^= __builtin_popcount(v & c.adjlo[q]);
-        return par & 1u;
-    };
-    c.qcol = 0;
-    for (uint32_t j = 0; j < 16; ++j) c.qcol |= qform(j) << j;
-    for (uint32_t r = 0; r < 256; ++r) {
-        const uint32_t v = r << 4;
-        uint32_t m = 0;
-        for (int q = 4; q < 12; ++q)
-            if ((v >> q) & 1u) m ^= c.adj[q] & 15u;
-        c.rowinfo[r] = static_cast<uint8_t>((qform(v) << 4) | m);
-    }
-    return c;
-}
-
 namespace {
 
 struct Builder {
@@ -162,58 +137,183 @@ Plan make_plan(const qf_gate *gates, size_t n_gates, uint32_t n, uint32_t n_para
     // CZ sets per stage (deduplicated) and the final one
     plan.stage_cz.assign(S, -1);
     std::vector<std::pair<uint32_t, uint32_t>> final_pairs;
+    auto adjacency = [&](const std::vector<std::pair<uint32_t, uint32_t>> &pairs) {
+        std::vector<uint32_t> adj(32, 0);
+        for (auto [x, y] : pairs) { // repeated CZ pairs cancel (parity)
+            adj[x] ^= 1u << y;
+            adj[y] ^= 1u << x;
+        }
+        return adj;
+    };
+    std::vector<std::vector<uint32_t>> adjs;
     auto intern = [&](const std::vector<std::pair<uint32_t, uint32_t>> &pairs) {
-        const CzSet c = make_czset(pairs);
-        for (size_t k = 0; k < plan.czsets.size(); ++k)
-            if (std::equal(std::begin(c.adj), std::end(c.adj), std::begin(plan.czsets[k].adj)))
-                return static_cast<int>(k);
-        plan.czsets.push_back(c);
-        return static_cast<int>(plan.czsets.size() - 1);
+        const auto a = adjacency(pairs);
+        for (size_t k = 0; k < adjs.size(); ++k)
+            if (adjs[k] == a) return static_cast<int>(k);
+        adjs.push_back(a);
+        plan.czsets.push_back(pairs);
+        return static_cast<int>(adjs.size() - 1);
     };
     for (auto &[t, pairs] : b.cz_at) {
         if (t >= S) final_pairs.insert(final_pairs.end(), pairs.begin(), pairs.end());
         else plan.stage_cz[t] = intern(pairs);
     }
-    if (!final_pairs.empty()) plan.final_cz = intern(final_pairs);
+    if (!final_pairs.empty()) {
+        const auto a = adjacency(final_pairs);
+        CzAdj f{};
+        for (int q = 0; q < 32; ++q) f.adjlo[q] = a[q] & ((1u << q) - 1u);
+        plan.final_adj.push_back(f);
+    }
 
-    // ---- schedule
+    // ---- layouts
     plan.resident = n <= static_cast<uint32_t>(kTileBits);
-    if (!plan.resident) {
-        PassLayout A{};
+    auto finish_layout = [&](PassLayout &L) {
+        // diag-group view: register bits, thread bits (other local bits in order), tile bits
+        for (int i = 0; i < 28; ++i) L.dq[i] = -1;
+        int t = 0;
+        for (int l = 0; l < 12; ++l) {
+            if (l / 4 == L.gd) L.dq[l % 4] = L.qmap[l];
+            else L.dq[4 + t++] = L.qmap[l];
+        }
+        for (size_t i = 0; i < L.tile_qubits.size() && i < 16; ++i) L.dq[12 + i] = L.tile_qubits[i];
+    };
+    if (plan.resident) {
+        PassLayout R;
+        R.row_start = 4;
+        for (int l = 0; l < 12; ++l) R.qmap[l] = l < static_cast<int>(n) ? l : -1;
+        R.rot_mask = (1u << std::min<uint32_t>(n, 12)) - 1u;
+        R.gd = 0;
+        finish_layout(R);
+        plan.layouts.push_back(R);
+    } else {
+        PassLayout A;
         A.row_start = 4;
         A.tile_lo_bits = 0;
         A.tile_hi_bits = static_cast<int>(n) - 12;
         A.rot_mask = 0xFFFu;
-        A.has_diag = true;
+        A.gd = 0;
         for (int l = 0; l < 12; ++l) A.qmap[l] = l;
-        plan.passes.push_back(A);
-        // remaining qubits 12..n-1 in 8-row blocks from the top
-        int hi = static_cast<int>(n); // rotate [lo, hi)
+        for (int q = 12; q < static_cast<int>(n); ++q) A.tile_qubits.push_back(q);
+        finish_layout(A);
+        plan.layouts.push_back(A);
+        int hi = static_cast<int>(n); // qubits [12, hi) still need a layout
         while (hi > 12) {
             const int a = std::max(4, hi - 8);
-            PassLayout P{};
+            PassLayout P;
             P.row_start = a;
             P.tile_lo_bits = a - 4;
             P.tile_hi_bits = static_cast<int>(n) - a - 8;
-            P.has_diag = false;
             for (int l = 0; l < 4; ++l) P.qmap[l] = l;
             for (int l = 4; l < 12; ++l) P.qmap[l] = a + (l - 4);
-            P.rot_mask = 0;
             for (int l = 4; l < 12; ++l)
                 if (P.qmap[l] >= 12 && P.qmap[l] < hi) P.rot_mask |= 1u << l;
-            plan.passes.push_back(P);
+            P.gd = (P.rot_mask & 0xF00u) ? 2 : 1;
+            for (int q = 4; q < a; ++q) P.tile_qubits.push_back(q);
+            for (int q = a + 8; q < static_cast<int>(n); ++q) P.tile_qubits.push_back(q);
+            finish_layout(P);
+            plan.layouts.push_back(P);
             hi = a;
         }
     }
-    // checkpoint interval in stages
+    const int NL = static_cast<int>(plan.layouts.size());
+
+    // ---- CZ sign tables per (CZ set, layout)
+    for (size_t c = 0; c < adjs.size(); ++c) {
+        const auto &adj = adjs[c];
+        for (int li = 0; li < NL; ++li) {
+            const PassLayout &L = plan.layouts[li];
+            auto qset = [&](const int *qs, int k, uint32_t v) { // Q of the set bits
+                uint32_t par = 0;
+                for (int i = 0; i < k; ++i) {
+                    if (!((v >> i) & 1u) || qs[i] < 0) continue;
+                    for (int j = i + 1; j < k; ++j)
+                        if (((v >> j) & 1u) && qs[j] >= 0) par ^= (adj[qs[i]] >> qs[j]) & 1u;
+                }
+                return par;
+            };
+            auto cross = [&](const int *qs, int k, uint32_t v, const int *to, int kto) {
+                uint32_t m = 0;
+                for (int i = 0; i < k; ++i) {
+                    if (!((v >> i) & 1u) || qs[i] < 0) continue;
+                    for (int r = 0; r < kto; ++r)
+                        if (to[r] >= 0) m ^= ((adj[qs[i]] >> to[r]) & 1u) << r;
+                }
+                return m;
+            };
+            const int *reg = L.dq, *thr = L.dq + 4;
+            CzTab ct{};
+            for (uint32_t j = 0; j < 16; ++j) ct.qreg |= qset(reg, 4, j) << j;
+            for (uint32_t tau = 0; tau < 256; ++tau)
+                ct.thrinfo[tau] = static_cast<uint16_t>((qset(thr, 8, tau) << 4) | cross(thr, 8, tau, reg, 4));
+            plan.cztab.push_back(ct);
+            const int kt = static_cast<int>(L.tile_qubits.size());
+            std::vector<uint32_t> ti(size_t(1) << kt);
+            for (uint32_t tb = 0; tb < ti.size(); ++tb)
+                ti[tb] = qset(L.tile_qubits.data(), kt, tb) | (cross(L.tile_qubits.data(), kt, tb, reg, 4) << 1) |
+                         (cross(L.tile_qubits.data(), kt, tb, thr, 8) << 8);
+            plan.tileinfo.push_back(std::move(ti));
+        }
+    }
+
+    // ---- pass sequence (streaming): a pass on layout X applies Ry_{r[X]}(X); when
+    // every layout has finished stage dnext-1 it also applies D_{dnext} and, on
+    // its own qubits, Ry_{dnext}. Two layouts -> one pass per stage.
+    plan.stage_layout.assign(S, 0);
+    if (!plan.resident && S > 0) {
+        std::vector<int> r(NL, 0);
+        int dnext = 0, X = 0;
+        auto all_done = [&](int st) {
+            for (int y = 0; y < NL; ++y)
+                if (r[y] < st) return false;
+            return true;
+        };
+        while (true) {
+            bool finished = true;
+            for (int y = 0; y < NL; ++y) finished &= r[y] >= S;
+            if (finished) break;
+            PassStep st;
+            st.layout = X;
+            if (r[X] < S && dnext > r[X]) st.s0 = r[X]++;
+            if (dnext < S && all_done(dnext)) {
+                st.sd = dnext;
+                plan.stage_layout[dnext] = X;
+                ++dnext;
+                if (r[X] < S && dnext > r[X]) st.s1 = r[X]++;
+            }
+            // phases: round-0 groups (gd last), then round-1 groups
+            const PassLayout &L = plan.layouts[X];
+            std::vector<int> groups;
+            for (int g = 0; g < 3; ++g)
+                if (g != L.gd && (L.rot_mask >> (4 * g)) & 0xFu) groups.push_back(g);
+            auto add = [&](int g, uint8_t ops) { st.ph[st.nph++] = PassPhase{int8_t(g), ops}; };
+            const uint8_t d_op = st.sd >= 0 ? 2 : 0;
+            if (st.s0 >= 0)
+                for (int g : groups) add(g, 1);
+            const uint8_t gd_ops = uint8_t((st.s0 >= 0 ? 1 : 0) | d_op | (st.s1 >= 0 ? 4 : 0));
+            if (gd_ops) add(L.gd, gd_ops);
+            if (st.s1 >= 0)
+                for (int g : groups) add(g, 4);
+            plan.steps.push_back(st);
+            X = (X + 1) % NL;
+        }
+    }
+
+    // checkpoint interval
     const uint32_t stages_per_layer =
         (layers > 0 && S % static_cast<int>(layers) == 0) ? static_cast<uint32_t>(S) / layers : 1u;
     uint32_t k = ckpt_layers ? ckpt_layers * stages_per_layer : std::min<uint32_t>(S ? S : 1, 10u);
     if (k == 0) k = 1;
     plan.ckpt_stages = k;
     plan.ckpt_layers = ckpt_layers ? ckpt_layers : k / std::max(1u, stages_per_layer);
-    const uint32_t blocks = S == 0 ? 1 : (static_cast<uint32_t>(S) + k - 1) / k;
-    plan.n_slots = plan.resident ? (blocks > 0 ? blocks - 1 : 0) : blocks;
+    if (plan.resident) {
+        const uint32_t blocks = S == 0 ? 1 : (static_cast<uint32_t>(S) + k - 1) / k;
+        plan.n_slots = blocks > 0 ? blocks - 1 : 0;
+    } else {
+        const uint32_t pps = static_cast<uint32_t>(std::max(1, NL - 1));
+        plan.ckpt_passes = k * pps;
+        const size_t np = plan.steps.size();
+        plan.n_slots = np == 0 ? 0 : static_cast<uint32_t>((np + plan.ckpt_passes - 1) / plan.ckpt_passes);
+    }
     return plan;
 }
 

@@ -5,6 +5,7 @@
 #include <cstdint>
 #include <stdexcept>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/qfuse_b200.h"
@@ -18,42 +19,58 @@ struct CapacityError : std::runtime_error {
     using std::runtime_error::runtime_error;
 };
 
+// Which 12 qubits a tile keeps resident, and how the rest index tiles.
 struct PassLayout {
-    int row_start;     // first qubit of the 8 row bits
-    int tile_lo_bits;  // bits between column and rows
-    int tile_hi_bits;  // bits above the rows
-    uint32_t rot_mask; // local bits rotated in this pass
-    int qmap[12];      // local bit -> qubit
-    bool has_diag;     // pass A
+    int row_start = 4;    // first qubit of the 8 row bits
+    int tile_lo_bits = 0; // tile bits between column and rows (qubits 4..row_start-1)
+    int tile_hi_bits = 0; // tile bits above the rows (qubits row_start+8..n-1)
+    uint32_t rot_mask = 0;// local bits rotated in this layout
+    int qmap[12] = {};    // local bit -> qubit (-1: sample bit, resident layout only)
+    int gd = 0;           // group phase that applies the diagonal
+    int dq[28] = {};      // diag-group view: qubit of reg 0..3, thr 0..7, tile 0..15
+    std::vector<int> tile_qubits;
+};
+
+// One forward pass: Ry_{s0}(X) -> D_{sd} -> Ry_{s1}(X) on layout X.
+struct PassStep {
+    int layout = 0;
+    int s0 = -1, s1 = -1, sd = -1;
+    int nph = 0;
+    PassPhase ph[6] = {};
 };
 
 struct Plan {
     uint32_t n = 0, n_params = 0, layers = 0, batch = 0;
     uint64_t x_mask = 0, z_mask = 0;
     uint32_t y_count = 0;
-    // stages and diagonals
+    // stages
     uint32_t stages = 0;
-    std::vector<CzSet> czsets;     // distinct CZ sets (index 0.. )
+    std::vector<std::vector<std::pair<uint32_t, uint32_t>>> czsets; // distinct CZ sets
     std::vector<int> stage_cz;     // [stages] -> czsets index or -1
-    int final_cz = -1;             // index or -1
+    int final_cz = -1;
     // sections (one per single-qubit run)
     std::vector<uint32_t> sec_q, sec_stage, sec_alpha_row, sec_off, sec_gates;
     // schedule
     bool resident = false;         // n <= 12: one kernel per gradient
-    std::vector<PassLayout> passes;// streaming: A, B, (C)
+    std::vector<PassLayout> layouts; // resident: [0]; streaming: A, B, (C)
+    std::vector<PassStep> steps;   // streaming forward passes
+    std::vector<int> stage_layout; // layout whose pass applies D_s
+    std::vector<CzTab> cztab;      // [czset][layout]
+    std::vector<std::vector<uint32_t>> tileinfo; // [czset][layout]
+    std::vector<CzAdj> final_adj;  // 0 or 1 entries
     uint32_t ckpt_stages = 1;      // k in stages
     uint32_t ckpt_layers = 0;      // k in layers as reported
+    uint32_t ckpt_passes = 1;      // k in passes (streaming)
     uint32_t n_slots = 0;
-    // per-gate comparator: flattened gates kept as given
-    std::vector<qf_gate> gates;
+    std::vector<qf_gate> gates;    // as given (per-gate comparator)
+
+    bool slot_pass(size_t p) const {
+        return (p + 1) % ckpt_passes == 0 || p + 1 == steps.size();
+    }
 };
 
-// Builds a plan (throws std::invalid_argument / CapacityError with the
-// reference's messages).
 Plan make_plan(const qf_gate *gates, size_t n_gates, uint32_t n_qubits, uint32_t n_params,
                uint32_t layers, uint32_t ckpt_layers, uint32_t batch, uint64_t x_mask,
                uint64_t z_mask);
-
-CzSet make_czset(const std::vector<std::pair<uint32_t, uint32_t>> &pairs);
 
 } // namespace qfb

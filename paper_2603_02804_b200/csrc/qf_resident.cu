@@ -1,0 +1,320 @@
+// Sample-resident kernel (n <= 12) and the observable step.
+//
+// n <= 12: one 4096-amplitude tile holds 2^(12-n) whole samples, so the
+// forward over every stage, the observable (expectation + adjoint seed) and
+// the adjoint backward run without leaving shared memory. HBM sees psi0 and
+// the checkpoint slots (used to re-anchor the psi uncompute every k stages).
+//
+// Observable (engine.cpp:346-435): lambda = 2 O' psi, E_s = <psi|O'|psi>,
+// with the circuit's final diagonal folded in, O' = D_f^dag O D_f.
+#include "qf_device.cuh"
+
+namespace qfb {
+namespace {
+
+using namespace dev;
+
+__device__ __forceinline__ uint32_t qform_adj(const CzAdj *cz, uint32_t v) {
+    uint32_t par = 0, w = v;
+    while (w) {
+        const int q = __ffs(w) - 1;
+        w &= w - 1;
+        par ^= __popc(v & cz->adjlo[q]);
+    }
+    return par & 1u;
+}
+
+// 2 * phase_O(t) * D_f(t) * conj(D_f(x)), t = x ^ X (pauli_phase engine.cpp:346-372).
+__device__ __forceinline__ float2 seed_factor(uint32_t x, uint64_t X, uint64_t Z, uint32_t y,
+                                              const double *wf, const CzAdj *czf) {
+    const uint32_t t = x ^ uint32_t(X);
+    double ang = 0.0;
+    uint32_t xm = uint32_t(X);
+    while (xm) {
+        const int q = __ffs(xm) - 1;
+        xm &= xm - 1;
+        ang += ((x >> q) & 1u) ? -wf[q] : wf[q];
+    }
+    uint32_t par = __popc(t & uint32_t(Z));
+    if (czf) par += qform_adj(czf, x) ^ qform_adj(czf, t);
+    double s, c;
+    sincos(ang, &s, &c);
+    double re = 2.0 * c, im = 2.0 * s;
+    if (par & 1u) {
+        re = -re;
+        im = -im;
+    }
+    double r2 = re, i2 = im;
+    switch (y & 3u) {
+    case 1: r2 = -im; i2 = re; break;
+    case 2: r2 = -re; i2 = -im; break;
+    case 3: r2 = im; i2 = -re; break;
+    default: break;
+    }
+    return make_float2(float(r2), float(i2));
+}
+// D_f(x) for the forward-state readout.
+__device__ __forceinline__ float2 dfinal(uint32_t x, int n, const double *wf, const CzAdj *czf) {
+    double ang = 0.0;
+    for (int q = 0; q < n; ++q)
+        if ((x >> q) & 1u) ang += wf[q];
+    double s, c;
+    sincos(ang, &s, &c);
+    if (czf && qform_adj(czf, x)) {
+        s = -s;
+        c = -c;
+    }
+    return make_float2(float(c), float(s));
+}
+
+// Streaming observable step (n > 12) / forward-state readout.
+__global__ void __launch_bounds__(kThreads) seed_kernel(const SeedParams p) {
+    const uint64_t dim = 1ull << p.n;
+    const uint32_t per_block = dim < kTileAmps ? uint32_t(dim) : uint32_t(kTileAmps);
+    const uint32_t chunks = uint32_t(dim / per_block);
+    const uint32_t s = blockIdx.x / chunks, chunk = blockIdx.x % chunks;
+    const float2 *psi = p.psi + s * dim;
+    float2 *lam = p.lam + s * dim;
+    double e = 0.0;
+    for (uint32_t k = threadIdx.x; k < per_block; k += kThreads) {
+        const uint32_t x = chunk * per_block + k;
+        if (p.apply_only) {
+            lam[x] = cmul(dfinal(x, p.n, p.wfinal, p.czfinal), psi[x]);
+            continue;
+        }
+        const uint32_t t = x ^ uint32_t(p.x_mask);
+        const float2 f = seed_factor(x, p.x_mask, p.z_mask, p.y_count, p.wfinal, p.czfinal);
+        const float2 pt = psi[t], px = psi[x];
+        const float2 l = cmul(f, pt);
+        lam[x] = l;
+        e += 0.5 * (double(px.x) * double(l.x) + double(px.y) * double(l.y));
+    }
+    if (p.apply_only) return;
+    __shared__ double red[kThreads / 32];
+#pragma unroll
+    for (int m = 16; m >= 1; m >>= 1) e += __shfl_xor_sync(0xffffffffu, e, m);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = e;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < kThreads / 32; ++w) t += red[w];
+        p.epart[size_t(s) * chunks + chunk] = t;
+    }
+}
+
+constexpr size_t kResAcc = size_t(8) * 2 * 12 * 8 * sizeof(double);
+constexpr size_t res_smem() {
+    return size_t(2) * kTileBytes + size_t(kTileAmps) * sizeof(double) + 64 +
+           2 * 24 * 16 /*rys*/ + 2 * 16 * 8 /*treg*/ + kResAcc + 1024;
+}
+
+__global__ void __launch_bounds__(kThreads, 2)
+    resident_kernel(const __grid_constant__ ResidentParams p,
+                    const __grid_constant__ CUtensorMap m_psi0,
+                    const __grid_constant__ CUtensorMap m_slots,
+                    const __grid_constant__ CUtensorMap m_out) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = align1024(smem_raw);
+    uint8_t *pt = smem, *lt = smem + kTileBytes;
+    double *es = reinterpret_cast<double *>(smem + 2 * kTileBytes);
+    uint8_t *tail = smem + 2 * kTileBytes + kTileAmps * sizeof(double);
+    uint64_t *mbar = reinterpret_cast<uint64_t *>(tail);
+    float4 *rys = reinterpret_cast<float4 *>(tail + 64);                  // [2 slots][24]
+    float2 *treg_s = reinterpret_cast<float2 *>(tail + 64 + 2 * 24 * 16); // [2 slots][16]
+    double *acc = reinterpret_cast<double *>(tail + 64 + 2 * 24 * 16 + 2 * 16 * 8);
+    const uint32_t tid = threadIdx.x, warp = tid >> 5;
+    const int n = p.n, S = p.stages;
+    const uint32_t rot = (n >= 12) ? 0xFFFu : ((1u << n) - 1u);
+    const uint32_t xmask = rot;
+    const int spt = kTileAmps >> (n < 12 ? n : 12);
+
+    for (uint32_t i = tid; i < kResAcc / 8; i += kThreads) acc[i] = 0.0;
+    if (tid < 48) { // round-0 halves stay identity
+        rys[tid] = make_float4(1.f, 1.f, 0.f, 0.f);
+    }
+    if (tid == 0) {
+        prefetch_map(&m_psi0);
+        prefetch_map(&m_slots);
+        mbar_init(&mbar[0], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    uint32_t phase = 0;
+    auto load_stage = [&](int s) { // stage data into slot s & 1 (threads 64..91)
+        const int sl = s & 1;
+        if (tid >= 64 && tid < 76) {
+            const int lb = tid - 64;
+            float4 v = make_float4(1.f, 1.f, 0.f, 0.f);
+            if (lb < n) {
+                const float2 cs = p.ry[size_t(s) * n + lb];
+                v = make_float4(cs.x, cs.x, cs.y, cs.y);
+            }
+            rys[sl * 24 + 12 + lb] = v;
+        } else if (tid >= 76 && tid < 92) {
+            treg_s[sl * 16 + (tid - 76)] = p.dt[s].treg[tid - 76];
+        }
+    };
+    auto env_for = [&](int s) {
+        PhaseEnv e;
+        const int sl = s & 1;
+        e.rys = rys + sl * 24;
+        e.rot = rot;
+        e.treg_s = treg_s + sl * 16;
+        e.acc_w = acc + warp * 2 * 12 * 8;
+        const int c = p.stage_cz[s];
+        const CzTab *cz = c >= 0 ? p.cztabs + c : nullptr;
+        e.d = diag_ctx(tid, p.dt[s].tthr[tid], cz ? cz->thrinfo[tid] : 0u, p.dt + s, cz, nullptr, 0u);
+        return e;
+    };
+
+    for (int t = blockIdx.x; t < p.tiles; t += gridDim.x) {
+        if (tid == 0) {
+            mbar_expect_tx(&mbar[0], kTileBytes);
+            tma_load3(pt, &m_psi0, &mbar[0], 0, t * 256, 0);
+        }
+        if (S > 0) load_stage(0);
+        mbar_wait(&mbar[0], phase);
+        phase ^= 1u;
+        __syncthreads();
+        // ---------------- forward over all stages
+        for (int s = 0; s < S; ++s) {
+            const PhaseEnv e = env_for(s);
+            phase_fwd<0>(pt, tid, 2u | 4u, e);
+            __syncthreads();
+            if (rot & 0xF0u) {
+                phase_fwd<1>(pt, tid, 4u, e);
+                __syncthreads();
+            }
+            if (rot & 0xF00u) phase_fwd<2>(pt, tid, 4u, e);
+            if (s + 1 < S) load_stage(s + 1);
+            const bool slot = ((s + 1) % p.ckpt == 0) && (s + 1 < S) && !p.forward_only;
+            if (slot) fence_async_smem();
+            __syncthreads();
+            if (slot) {
+                if (tid == 0) {
+                    tma_store3(&m_slots, pt, 0, t * 256, (s + 1) / p.ckpt - 1);
+                    bulk_commit();
+                    bulk_wait_read0();
+                }
+                __syncthreads();
+            }
+        }
+        if (p.forward_only) { // fold D_f and store the final state
+#pragma unroll 4
+            for (int j = 0; j < 16; ++j) {
+                const uint32_t l = (tid << 4) | uint32_t(j);
+                float2 *a = reinterpret_cast<float2 *>(pt + swz(l));
+                *a = cmul(dfinal(l & xmask, n, p.wfinal, p.czfinal), *a);
+            }
+            fence_async_smem();
+            __syncthreads();
+            if (tid == 0) {
+                tma_store3(&m_out, pt, 0, t * 256, 0);
+                bulk_commit();
+                bulk_wait_read0();
+            }
+            __syncthreads();
+            continue;
+        }
+        // ---------------- observable: lambda = 2 O' psi, E per sample
+#pragma unroll 4
+        for (int j = 0; j < 16; ++j) {
+            const uint32_t l = (tid << 4) | uint32_t(j);
+            const uint32_t lp = l ^ uint32_t(p.x_mask);
+            const float2 f = seed_factor(l & xmask, p.x_mask, p.z_mask, p.y_count, p.wfinal, p.czfinal);
+            const float2 ps = *reinterpret_cast<const float2 *>(pt + swz(lp));
+            const float2 px = *reinterpret_cast<const float2 *>(pt + swz(l));
+            const float2 lv = cmul(f, ps);
+            *reinterpret_cast<float2 *>(lt + swz(l)) = lv;
+            es[l] = 0.5 * (double(px.x) * double(lv.x) + double(px.y) * double(lv.y));
+        }
+        __syncthreads();
+        for (int st = 1; st < (1 << (n < 12 ? n : 12)); st <<= 1) {
+            for (int i = tid; i < (kTileAmps >> 1) / st; i += kThreads) {
+                const int idx = i * 2 * st;
+                es[idx] += es[idx + st];
+            }
+            __syncthreads();
+        }
+        if (tid < uint32_t(spt)) {
+            const uint64_t sample = uint64_t(t) * spt + tid;
+            if (sample < p.batch) p.expect[sample] = es[tid << (n < 12 ? n : 12)];
+        }
+        // ---------------- backward
+        if (S > 0) load_stage(S - 1);
+        __syncthreads();
+        for (int s = S - 1; s >= 0; --s) {
+            if (((s + 1) % p.ckpt == 0) && (s + 1 < S)) { // re-anchor psi at the slot
+                if (tid == 0) {
+                    mbar_expect_tx(&mbar[0], kTileBytes);
+                    tma_load3(pt, &m_slots, &mbar[0], 0, t * 256, (s + 1) / p.ckpt - 1);
+                }
+                mbar_wait(&mbar[0], phase);
+                phase ^= 1u;
+            }
+            const PhaseEnv e = env_for(s);
+            if (rot & 0xF00u) {
+                phase_bwd<2>(pt, lt, tid, 4u, e);
+                __syncthreads();
+            }
+            if (rot & 0xF0u) {
+                phase_bwd<1>(pt, lt, tid, 4u, e);
+                __syncthreads();
+            }
+            phase_bwd<0>(pt, lt, tid, 4u | 2u, e);
+            if (s > 0) load_stage(s - 1);
+            __syncthreads();
+            if (tid < 96) {
+                const int lb = tid >> 3, c = tid & 7;
+                if (lb < n) {
+                    double sum = 0.0;
+#pragma unroll
+                    for (int w = 0; w < 8; ++w) {
+                        double *a = acc + ((w * 2 + 1) * 12 + lb) * 8 + c;
+                        sum += *a;
+                        *a = 0.0;
+                    }
+                    p.kpart[(size_t(blockIdx.x) * S + s) * size_t(n) * 8 + lb * 8 + c] += sum;
+                }
+            }
+            __syncthreads();
+        }
+    }
+    if (tid == 0) bulk_wait0();
+}
+
+bool g_attrs = false;
+
+} // namespace
+
+size_t resident_smem_bytes() { return res_smem(); }
+
+int resident_occupancy() {
+    if (!g_attrs) {
+        if (cudaFuncSetAttribute(resident_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(res_smem())) != cudaSuccess)
+            return 0;
+        g_attrs = true;
+    }
+    int blocks = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, resident_kernel, kThreads, res_smem());
+    return blocks;
+}
+
+cudaError_t launch_resident(cudaStream_t st, int grid, const ResidentParams &p,
+                            const CUtensorMap *psi0, const CUtensorMap *slots_map,
+                            const CUtensorMap *out_map) {
+    if (resident_occupancy() <= 0) return cudaErrorInvalidConfiguration;
+    resident_kernel<<<grid, kThreads, res_smem(), st>>>(p, *psi0, *slots_map, *out_map);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_seed(cudaStream_t st, const SeedParams &p) {
+    const uint64_t dim = 1ull << p.n;
+    const uint64_t per_block = dim < kTileAmps ? dim : kTileAmps;
+    const uint64_t blocks = (dim / per_block) * p.batch;
+    seed_kernel<<<unsigned(blocks), kThreads, 0, st>>>(p);
+    return cudaGetLastError();
+}
+
+} // namespace qfb

@@ -1,0 +1,44 @@
+"""CPU: the C-ABI library loads and exports every entry point declared in
+include/qfuse_b200.h (no compute without a GPU)."""
+import ctypes
+import os
+import re
+
+import paper_2603_02804_b200 as pkg
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "qfuse_b200.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(qf_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_header_symbols_exported():
+    lib = pkg.load()
+    declared = _declared()
+    assert len(declared) >= 20
+    missing = [s for s in declared if not hasattr(lib, s)]
+    assert not missing, missing
+    assert set(pkg.SYMBOLS) == set(declared)
+
+
+def test_version_and_no_device_error():
+    lib = pkg.load()
+    assert b"sm_100a" in lib.qf_version()
+    h = ctypes.c_void_p()
+    rc = lib.qf_ctx_create(0, ctypes.byref(h))
+    if rc == 0:  # a B200 is visible (GPU box)
+        assert lib.qf_ctx_destroy(h) == 0
+    else:        # no device here: a clean error, never a crash or a CPU fallback
+        assert rc == pkg.capi.QF_EDEVICE or rc == pkg.capi.QF_EINVAL
+        assert lib.qf_last_error()
+
+
+def test_library_is_sm100a_only():
+    import subprocess
+    out = subprocess.run(["cuobjdump", "--list-elf", pkg.LIB_PATH], capture_output=True,
+                         text=True).stdout
+    assert "sm_100a" in out
+    assert "sm_90" not in out and "sm_80" not in out

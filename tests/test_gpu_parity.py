@@ -142,3 +142,49 @@ def test_errors(ctx):
     with pytest.raises(capi.QfCapacityError):
         g26, np26 = C.build_hea(26, 1)
         capi.Plan(ctx, g26, 26, np26, 1, 0, 1 << 12, C.parse_pauli("Z" * 26))
+
+
+@pytest.mark.parametrize("n,layers,batch", [(4, 3, 5), (12, 2, 2), (14, 2, 2), (17, 2, 1)])
+def test_forward_state_matches_reference(ctx, ref, n, layers, batch):
+    """Final state of the fused forward vs the reference's forward<double>,
+    up to one global phase per sample (the device drops e^{i delta})."""
+    gates, npar, theta, psi0, pauli = _hea_case(n, layers, batch, seed=41)
+    plan = capi.Plan(ctx, gates, n, npar, layers, 0, batch, pauli)
+    plan.upload_psi0(psi0)
+    got = plan.forward_state(theta).astype(np.float64)
+    want = ref.forward(gates, n, npar, psi0.astype(np.float64), theta)
+    g = got[..., 0] + 1j * got[..., 1]
+    w = want[..., 0] + 1j * want[..., 1]
+    for s in range(batch):
+        ov = np.vdot(g[s], w[s])
+        assert abs(abs(ov) - 1.0) < 1e-5
+        ph = ov / abs(ov)
+        assert np.max(np.abs(g[s] * ph - w[s])) < 1e-5
+
+
+@pytest.mark.parametrize("n,layers,batch", [(21, 1, 1), (22, 2, 1)])
+def test_three_layouts(ctx, oracle, n, layers, batch):
+    """n > 20 needs a third layout (two passes per stage)."""
+    gates, npar, theta, psi0, pauli = _hea_case(n, layers, batch, seed=8)
+    res = capi.gradient_c64(ctx, gates, n, npar, layers, 0, psi0, theta, pauli)
+    _check(res, oracle.gradient(gates, n, npar, psi0, theta, pauli))
+
+
+@pytest.mark.parametrize("k", [1, 2, 3, 6])
+def test_streaming_checkpoint_slots(ctx, oracle, k):
+    n, layers = 15, 6
+    gates, npar, theta, psi0, pauli = _hea_case(n, layers, 2, seed=17)
+    res = capi.gradient_c64(ctx, gates, n, npar, layers, k, psi0, theta, pauli)
+    _check(res, oracle.gradient(gates, n, npar, psi0, theta, pauli))
+
+
+def test_device_random_state(ctx):
+    """qf_plan_random_psi0 == new_random_state<float> (statevec.cpp:32-53)."""
+    n, batch = 13, 3
+    gates, npar = C.build_hea(n, 1)
+    plan = capi.Plan(ctx, gates, n, npar, 1, 0, batch, C.parse_pauli("Z" * n))
+    plan.random_psi0(1234, first_sample=5)
+    host = np.empty((batch, 1 << n, 2), np.float32)
+    plan.download_psi0_ptr(host.ctypes.data)
+    want = C.new_random_state(n, 5 + batch, 1234)[5:]
+    np.testing.assert_allclose(host, want, rtol=0, atol=2e-7)
