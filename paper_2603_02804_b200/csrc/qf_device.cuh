@@ -82,9 +82,11 @@ __device__ __forceinline__ void fence_async_smem() {
 __device__ __forceinline__ void prefetch_map(const CUtensorMap *m) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
 }
+// Align a dynamic-smem pointer to 1024 B (SWIZZLE_128B) by pointer arithmetic
+// on the shared pointer itself, so the compiler keeps the shared address space
+// (LDS/STS, not generic LD/ST).
 __device__ __forceinline__ uint8_t *align1024(uint8_t *p) {
-    const uintptr_t a = reinterpret_cast<uintptr_t>(p);
-    return reinterpret_cast<uint8_t *>((a + 1023) & ~uintptr_t(1023));
+    return p + ((1024u - (su32(p) & 1023u)) & 1023u);
 }
 
 // ------------------------------------------------------- tile addressing
@@ -106,30 +108,53 @@ __device__ __forceinline__ uint32_t swz(uint32_t l) {
     const uint32_t r = l >> 4, c = l & 15u;
     return (r << 7) | ((((c >> 1) ^ r) & 7u) << 4) | ((c & 1u) << 3);
 }
+// Explicit shared-space accesses (LDS/STS) on 32-bit shared addresses, so no
+// code path can fall back to generic LD/ST.
+__device__ __forceinline__ float2 lds64(uint32_t a) {
+    float2 v;
+    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ float4 lds128(uint32_t a) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void sts64(uint32_t a, float2 v) {
+    asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(a), "f"(v.x), "f"(v.y) : "memory");
+}
+__device__ __forceinline__ void sts128(uint32_t a, float4 v) {
+    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z),
+                 "f"(v.w)
+                 : "memory");
+}
 template <int G>
 __device__ __forceinline__ void lds16(const uint8_t *tile, uint32_t tau, float2 (&v)[16]) {
+    const uint32_t base = su32(tile);
     if (G == 0) {
 #pragma unroll
         for (int j = 0; j < 16; j += 2) {
-            const float4 t = *reinterpret_cast<const float4 *>(tile + goff<0>(tau, j));
+            const float4 t = lds128(base + goff<0>(tau, j));
             v[j] = make_float2(t.x, t.y);
             v[j + 1] = make_float2(t.z, t.w);
         }
     } else {
 #pragma unroll
-        for (int j = 0; j < 16; ++j) v[j] = *reinterpret_cast<const float2 *>(tile + goff<G>(tau, j));
+        for (int j = 0; j < 16; ++j) v[j] = lds64(base + goff<G>(tau, j));
     }
 }
 template <int G>
 __device__ __forceinline__ void sts16(uint8_t *tile, uint32_t tau, const float2 (&v)[16]) {
+    const uint32_t base = su32(tile);
     if (G == 0) {
 #pragma unroll
         for (int j = 0; j < 16; j += 2)
-            *reinterpret_cast<float4 *>(tile + goff<0>(tau, j)) =
-                make_float4(v[j].x, v[j].y, v[j + 1].x, v[j + 1].y);
+            sts128(base + goff<0>(tau, j), make_float4(v[j].x, v[j].y, v[j + 1].x, v[j + 1].y));
     } else {
 #pragma unroll
-        for (int j = 0; j < 16; ++j) *reinterpret_cast<float2 *>(tile + goff<G>(tau, j)) = v[j];
+        for (int j = 0; j < 16; ++j) sts64(base + goff<G>(tau, j), v[j]);
     }
 }
 
@@ -160,13 +185,15 @@ __device__ __forceinline__ void ry2(float2 (&v)[16], float4 cs) {
         v[j | (1 << B)] = f2fma(S, a, f2mul(C, b));
     }
 }
-// One Ry round on the rotated bits of group G (warp-uniform branches).
-template <int G, bool INV>
+// One Ry round on the rotated bits of group G. FULL (all four bits rotated,
+// the HEA case) is branch-free so the register array never has to be merged
+// across control flow; otherwise warp-uniform branches per bit.
+template <int G, bool INV, bool FULL>
 __device__ __forceinline__ void ry_round(float2 (&v)[16], const float4 *rys, uint32_t rot) {
-    if (rot & (1u << (4 * G + 0))) ry2<0, INV>(v, rys[4 * G + 0]);
-    if (rot & (1u << (4 * G + 1))) ry2<1, INV>(v, rys[4 * G + 1]);
-    if (rot & (1u << (4 * G + 2))) ry2<2, INV>(v, rys[4 * G + 2]);
-    if (rot & (1u << (4 * G + 3))) ry2<3, INV>(v, rys[4 * G + 3]);
+    if (FULL || (rot & (1u << (4 * G + 0)))) ry2<0, INV>(v, rys[4 * G + 0]);
+    if (FULL || (rot & (1u << (4 * G + 1)))) ry2<1, INV>(v, rys[4 * G + 1]);
+    if (FULL || (rot & (1u << (4 * G + 2)))) ry2<2, INV>(v, rys[4 * G + 2]);
+    if (FULL || (rot & (1u << (4 * G + 3)))) ry2<3, INV>(v, rys[4 * G + 3]);
 }
 
 // K_ab = sum psi_a conj(lam_b) over the pairs of register bit B, written as
@@ -217,25 +244,50 @@ __device__ __forceinline__ float warp_reduce_scatter32(float (&v)[32]) {
     return v[0];
 }
 
+// Reduce 8 per-lane values over the warp: lane L ends with the sum of value
+// L & 7 (7 + 2 shuffles).
+__device__ __forceinline__ float warp_reduce8(float (&v)[8]) {
+    const uint32_t lane = threadIdx.x & 31u;
+#pragma unroll
+    for (int m = 4; m >= 1; m >>= 1) {
+        const bool up = (lane & m) != 0;
+#pragma unroll
+        for (int i = 0; i < m; ++i) {
+            const float send = up ? v[i] : v[i + m];
+            const float keep = up ? v[i + m] : v[i];
+            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, m);
+        }
+    }
+    float r = v[0];
+    r += __shfl_xor_sync(0xffffffffu, r, 8);
+    r += __shfl_xor_sync(0xffffffffu, r, 16);
+    return r;
+}
+
+template <int G, int B, bool FULL>
+__device__ __forceinline__ void kmeasure_bit(const float2 (&p)[16], const float2 (&ps)[16],
+                                             const float2 (&l)[16], uint32_t rot, double *acc_w) {
+    if (!FULL && !(rot & (1u << (4 * G + B)))) return;
+    float k[8];
+    kbit<B>(p, ps, l, k);
+    const float r = warp_reduce8(k);
+    const uint32_t lane = threadIdx.x & 31u;
+    if (lane < 8) acc_w[(4 * G + B) * 8 + lane] += double(r);
+}
+
 // K of every rotated bit of group G at the current point, added (fp64) to
-// this warp's accumulator acc_w[local bit][8].
-template <int G>
+// this warp's accumulator acc_w[local bit][8]; one bit at a time keeps the
+// live accumulators at 8.
+template <int G, bool FULL>
 __device__ __forceinline__ void kmeasure(const float2 (&p)[16], const float2 (&l)[16],
                                          uint32_t rot, double *acc_w) {
-    if (!(rot & (0xFu << (4 * G)))) return;
     float2 ps[16];
 #pragma unroll
     for (int j = 0; j < 16; ++j) ps[j] = make_float2(p[j].y, p[j].x);
-    float k[32];
-#pragma unroll
-    for (int i = 0; i < 32; ++i) k[i] = 0.f;
-    if (rot & (1u << (4 * G + 0))) kbit<0>(p, ps, l, k + 0);
-    if (rot & (1u << (4 * G + 1))) kbit<1>(p, ps, l, k + 8);
-    if (rot & (1u << (4 * G + 2))) kbit<2>(p, ps, l, k + 16);
-    if (rot & (1u << (4 * G + 3))) kbit<3>(p, ps, l, k + 24);
-    const float r = warp_reduce_scatter32(k);
-    const uint32_t lane = threadIdx.x & 31u;
-    if (rot & (1u << (4 * G + (lane >> 3)))) acc_w[(4 * G + (lane >> 3)) * 8 + (lane & 7u)] += double(r);
+    kmeasure_bit<G, 0, FULL>(p, ps, l, rot, acc_w);
+    kmeasure_bit<G, 1, FULL>(p, ps, l, rot, acc_w);
+    kmeasure_bit<G, 2, FULL>(p, ps, l, rot, acc_w);
+    kmeasure_bit<G, 3, FULL>(p, ps, l, rot, acc_w);
 }
 
 // ------------------------------------------------------------- diagonal
@@ -287,51 +339,74 @@ struct PhaseEnv {
     const float2 *treg_s;
     double *acc_w;     // this warp's [2 rounds][12][8] accumulators
 };
-// ops: 1 = round 0, 2 = diagonal, 4 = round 1.
-template <int G>
-__device__ __forceinline__ void phase_fwd(uint8_t *tile, uint32_t tau, uint32_t ops,
-                                          const PhaseEnv &e) {
+// OPS: 1 = round 0, 2 = diagonal, 4 = round 1 (compile-time, so the 16-register
+// arrays stay in place across the whole phase).
+template <int G, uint32_t OPS, bool FULL>
+__device__ __forceinline__ void phase_fwd(uint8_t *tile, uint32_t tau, const PhaseEnv &e) {
     float2 v[16];
     lds16<G>(tile, tau, v);
-    if (ops & 1u) ry_round<G, false>(v, e.rys, e.rot);
-    if (ops & 2u) apply_diag<false>(v, e.d, e.treg_s);
-    if (ops & 4u) ry_round<G, false>(v, e.rys + 12, e.rot);
+    if (OPS & 1u) ry_round<G, false, FULL>(v, e.rys, e.rot);
+    if (OPS & 2u) apply_diag<false>(v, e.d, e.treg_s);
+    if (OPS & 4u) ry_round<G, false, FULL>(v, e.rys + 12, e.rot);
     sts16<G>(tile, tau, v);
 }
-template <int G>
-__device__ __forceinline__ void phase_bwd(uint8_t *pt, uint8_t *lt, uint32_t tau, uint32_t ops,
-                                          const PhaseEnv &e) {
+template <int G, uint32_t OPS, bool FULL>
+__device__ __forceinline__ void phase_bwd(uint8_t *pt, uint8_t *lt, uint32_t tau, const PhaseEnv &e) {
     float2 p[16], l[16];
     lds16<G>(pt, tau, p);
     lds16<G>(lt, tau, l);
-    if (ops & 4u) {
-        ry_round<G, true>(p, e.rys + 12, e.rot);
-        ry_round<G, true>(l, e.rys + 12, e.rot);
-        kmeasure<G>(p, l, e.rot, e.acc_w + 12 * 8);
+    if (OPS & 4u) {
+        ry_round<G, true, FULL>(p, e.rys + 12, e.rot);
+        ry_round<G, true, FULL>(l, e.rys + 12, e.rot);
+        kmeasure<G, FULL>(p, l, e.rot, e.acc_w + 12 * 8);
     }
-    if (ops & 2u) {
+    if (OPS & 2u) {
         apply_diag<true>(p, e.d, e.treg_s);
         apply_diag<true>(l, e.d, e.treg_s);
     }
-    if (ops & 1u) {
-        ry_round<G, true>(p, e.rys, e.rot);
-        ry_round<G, true>(l, e.rys, e.rot);
-        kmeasure<G>(p, l, e.rot, e.acc_w);
+    if (OPS & 1u) {
+        ry_round<G, true, FULL>(p, e.rys, e.rot);
+        ry_round<G, true, FULL>(l, e.rys, e.rot);
+        kmeasure<G, FULL>(p, l, e.rot, e.acc_w);
     }
     sts16<G>(pt, tau, p);
     sts16<G>(lt, tau, l);
 }
+
+// Runtime (group, ops, full) -> template instance. ops in {1, 4, 2|4, 1|2|4}.
+template <int G, bool FULL>
+__device__ __forceinline__ void run_fwd_g(uint32_t ops, uint8_t *tile, uint32_t tau,
+                                          const PhaseEnv &e) {
+    switch (ops) {
+    case 1: phase_fwd<G, 1, FULL>(tile, tau, e); break;
+    case 4: phase_fwd<G, 4, FULL>(tile, tau, e); break;
+    case 6: phase_fwd<G, 6, FULL>(tile, tau, e); break;
+    default: phase_fwd<G, 7, FULL>(tile, tau, e); break;
+    }
+}
+template <int G, bool FULL>
+__device__ __forceinline__ void run_bwd_g(uint32_t ops, uint8_t *pt, uint8_t *lt, uint32_t tau,
+                                          const PhaseEnv &e) {
+    switch (ops) {
+    case 1: phase_bwd<G, 1, FULL>(pt, lt, tau, e); break;
+    case 4: phase_bwd<G, 4, FULL>(pt, lt, tau, e); break;
+    case 6: phase_bwd<G, 6, FULL>(pt, lt, tau, e); break;
+    default: phase_bwd<G, 7, FULL>(pt, lt, tau, e); break;
+    }
+}
 __device__ __forceinline__ void run_phase_fwd(int g, uint8_t *tile, uint32_t tau, uint32_t ops,
                                               const PhaseEnv &e) {
-    if (g == 0) phase_fwd<0>(tile, tau, ops, e);
-    else if (g == 1) phase_fwd<1>(tile, tau, ops, e);
-    else phase_fwd<2>(tile, tau, ops, e);
+    const bool full = ((e.rot >> (4 * g)) & 0xFu) == 0xFu;
+    if (g == 0) full ? run_fwd_g<0, true>(ops, tile, tau, e) : run_fwd_g<0, false>(ops, tile, tau, e);
+    else if (g == 1) full ? run_fwd_g<1, true>(ops, tile, tau, e) : run_fwd_g<1, false>(ops, tile, tau, e);
+    else full ? run_fwd_g<2, true>(ops, tile, tau, e) : run_fwd_g<2, false>(ops, tile, tau, e);
 }
 __device__ __forceinline__ void run_phase_bwd(int g, uint8_t *pt, uint8_t *lt, uint32_t tau,
                                               uint32_t ops, const PhaseEnv &e) {
-    if (g == 0) phase_bwd<0>(pt, lt, tau, ops, e);
-    else if (g == 1) phase_bwd<1>(pt, lt, tau, ops, e);
-    else phase_bwd<2>(pt, lt, tau, ops, e);
+    const bool full = ((e.rot >> (4 * g)) & 0xFu) == 0xFu;
+    if (g == 0) full ? run_bwd_g<0, true>(ops, pt, lt, tau, e) : run_bwd_g<0, false>(ops, pt, lt, tau, e);
+    else if (g == 1) full ? run_bwd_g<1, true>(ops, pt, lt, tau, e) : run_bwd_g<1, false>(ops, pt, lt, tau, e);
+    else full ? run_bwd_g<2, true>(ops, pt, lt, tau, e) : run_bwd_g<2, false>(ops, pt, lt, tau, e);
 }
 
 } // namespace dev

@@ -18,21 +18,25 @@ using namespace dev;
 
 constexpr size_t kAccBytes = size_t(8) * 2 * 12 * 8 * sizeof(double); // [warp][round][bit][8]
 
+// Forward: 3 CTAs/SM, each double-buffered (load of tile i+1 overlaps tile i).
+// Backward: 2 CTAs/SM, single-buffered (psi + lambda = 64 KiB); the two CTAs
+// overlap each other's TMA traffic with compute.
+constexpr int nbuf(bool bwd) { return bwd ? 1 : 2; }
 constexpr size_t pass_smem(bool bwd) {
-    return size_t(2) * kTileBytes * (bwd ? 2 : 1) + 64 /*mbar*/ + 24 * 16 /*rys*/ +
+    return size_t(nbuf(bwd)) * kTileBytes * (bwd ? 2 : 1) + 64 /*mbar*/ + 24 * 16 /*rys*/ +
            16 * 8 /*treg*/ + (bwd ? kAccBytes : 0) + 1024 /*align*/;
 }
 
 template <bool BWD>
-__global__ void __launch_bounds__(kThreads, BWD ? 1 : 2)
+__global__ void __launch_bounds__(kThreads, BWD ? 2 : 3)
     pass_kernel(const __grid_constant__ PassParams p, const __grid_constant__ CUtensorMap m_in,
                 const __grid_constant__ CUtensorMap m_out,
                 const __grid_constant__ CUtensorMap m_lam) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = align1024(smem_raw);
     constexpr uint32_t kBuf = uint32_t(kTileBytes) * (BWD ? 2 : 1);
-    uint8_t *buf[2] = {smem, smem + kBuf};
-    uint8_t *tail = smem + 2 * kBuf;
+    constexpr int NB = nbuf(BWD);
+    uint8_t *tail = smem + NB * kBuf;
     uint64_t *mbar = reinterpret_cast<uint64_t *>(tail);
     float4 *rys = reinterpret_cast<float4 *>(tail + 64);
     float2 *treg_s = reinterpret_cast<float2 *>(tail + 64 + 24 * 16);
@@ -71,14 +75,15 @@ __global__ void __launch_bounds__(kThreads, BWD ? 1 : 2)
     const uint32_t tis_mask = (1u << sample_shift) - 1u;
     auto issue_load = [&](int t, int b) {
         const int c1 = t & lo_mask, c3 = (t >> p.tile_lo_bits) & hi_mask, c4 = t >> sample_shift;
+        uint8_t *dst = smem + b * kBuf;
         mbar_expect_tx(&mbar[b], kBuf);
-        tma_load5(buf[b], &m_in, &mbar[b], 0, c1, 0, c3, c4);
-        if (BWD) tma_load5(buf[b] + kTileBytes, &m_lam, &mbar[b], 0, c1, 0, c3, c4);
+        tma_load5(dst, &m_in, &mbar[b], 0, c1, 0, c3, c4);
+        if (BWD) tma_load5(dst + kTileBytes, &m_lam, &mbar[b], 0, c1, 0, c3, c4);
     };
     const int stride = gridDim.x;
     if (tid == 0) {
-        if (int(blockIdx.x) < p.tiles) issue_load(blockIdx.x, 0);
-        if (int(blockIdx.x) + stride < p.tiles) issue_load(blockIdx.x + stride, 1);
+        for (int b = 0; b < NB; ++b)
+            if (int(blockIdx.x) + b * stride < p.tiles) issue_load(blockIdx.x + b * stride, b);
     }
     PhaseEnv env;
     env.rys = rys;
@@ -89,10 +94,10 @@ __global__ void __launch_bounds__(kThreads, BWD ? 1 : 2)
     env.d.sgn = 0;
     int it = 0;
     for (int t = blockIdx.x; t < p.tiles; t += stride, ++it) {
-        const int b = it & 1;
+        const int b = NB == 1 ? 0 : (it & 1);
         if (p.dt) env.d = diag_ctx(tid, tthr, thrinfo, p.dt, p.cz, p.tileinfo, uint32_t(t) & tis_mask);
-        mbar_wait(&mbar[b], (it >> 1) & 1);
-        uint8_t *pt = buf[b];
+        mbar_wait(&mbar[b], (it / NB) & 1);
+        uint8_t *pt = smem + b * kBuf;
         if (!BWD) {
             for (int i = 0; i < p.nph; ++i) {
                 if (i) __syncthreads();
@@ -111,7 +116,7 @@ __global__ void __launch_bounds__(kThreads, BWD ? 1 : 2)
             if (!BWD || p.write_psi) tma_store5(&m_out, pt, 0, c1, 0, c3, c4);
             if (BWD) tma_store5(&m_lam, pt + kTileBytes, 0, c1, 0, c3, c4);
             bulk_commit();
-            const int tn = t + 2 * stride;
+            const int tn = t + NB * stride;
             if (tn < p.tiles) {
                 bulk_wait_read0();
                 issue_load(tn, b);

@@ -179,13 +179,13 @@ __global__ void __launch_bounds__(kThreads, 2)
         // ---------------- forward over all stages
         for (int s = 0; s < S; ++s) {
             const PhaseEnv e = env_for(s);
-            phase_fwd<0>(pt, tid, 2u | 4u, e);
+            run_phase_fwd(0, pt, tid, 2u | 4u, e);
             __syncthreads();
             if (rot & 0xF0u) {
-                phase_fwd<1>(pt, tid, 4u, e);
+                run_phase_fwd(1, pt, tid, 4u, e);
                 __syncthreads();
             }
-            if (rot & 0xF00u) phase_fwd<2>(pt, tid, 4u, e);
+            if (rot & 0xF00u) run_phase_fwd(2, pt, tid, 4u, e);
             if (s + 1 < S) load_stage(s + 1);
             const bool slot = ((s + 1) % p.ckpt == 0) && (s + 1 < S) && !p.forward_only;
             if (slot) fence_async_smem();
@@ -254,14 +254,14 @@ __global__ void __launch_bounds__(kThreads, 2)
             }
             const PhaseEnv e = env_for(s);
             if (rot & 0xF00u) {
-                phase_bwd<2>(pt, lt, tid, 4u, e);
+                run_phase_bwd(2, pt, lt, tid, 4u, e);
                 __syncthreads();
             }
             if (rot & 0xF0u) {
-                phase_bwd<1>(pt, lt, tid, 4u, e);
+                run_phase_bwd(1, pt, lt, tid, 4u, e);
                 __syncthreads();
             }
-            phase_bwd<0>(pt, lt, tid, 4u | 2u, e);
+            run_phase_bwd(0, pt, lt, tid, 4u | 2u, e);
             if (s > 0) load_stage(s - 1);
             __syncthreads();
             if (tid < 96) {
