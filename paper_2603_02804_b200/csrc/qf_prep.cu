@@ -139,31 +139,31 @@ __global__ void reduce_kernel(long long entries, int grid, const double *kpart, 
     }
 }
 
+// loss = sum_s E_s (engine.cpp:733-738), fixed-order warp reduction.
+__global__ void loss_kernel(const double *expect, uint32_t batch, double *loss) {
+    double s = 0.0;
+    for (uint32_t i = threadIdx.x; i < batch; i += 32) s += expect[i];
+#pragma unroll
+    for (int m = 16; m >= 1; m >>= 1) s += __shfl_xor_sync(0xffffffffu, s, m);
+    if (threadIdx.x == 0) *loss = s;
+}
+
 // One thread per section: K at the point before Ry(beta) -> K at the run
 // start (Rz(gamma)^dag), then walk the run's gates: grad = Re Tr(dg K g^dag),
-// K <- g K g^dag. Last block: loss = sum_s E_s (engine.cpp:733-738).
+// K <- g K g^dag. K11 = tr K - K00 with tr K = sum psi conj(lam) = 2 loss
+// (invariant along the circuit; the pass kernels do not accumulate it).
 __global__ void finalize_kernel(int n_sec, const uint32_t *sec_q, const uint32_t *sec_stage,
                                 const uint32_t *sec_off, const uint32_t *sec_gates,
                                 const double *sec_gamma, const double *theta, int n,
-                                const double *kout, double *grad, const double *expect,
-                                uint32_t batch, double *loss) {
-    if (blockIdx.x == gridDim.x - 1) {
-        if (threadIdx.x < 32) {
-            double s = 0.0;
-            for (uint32_t i = threadIdx.x; i < batch; i += 32) s += expect[i];
-#pragma unroll
-            for (int m = 16; m >= 1; m >>= 1) s += __shfl_xor_sync(0xffffffffu, s, m);
-            if (threadIdx.x == 0) *loss = s;
-        }
-        return;
-    }
+                                const double *kout, double *grad, const double *loss) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n_sec) return;
     const double *k = kout + (size_t(sec_stage[i]) * n + sec_q[i]) * 8;
     const double g = sec_gamma[i];
     const double2 e = make_double2(cos(g), sin(g));
+    const double tr = 2.0 * (*loss);
     M2 K{{k[0], k[1]}, zmul(make_double2(k[2], k[3]), e), zmul(make_double2(k[4], k[5]), zconj(e)),
-         {k[6], k[7]}};
+         {tr - k[0], -k[1]}};
     for (uint32_t j = sec_off[i]; j < sec_off[i + 1]; ++j) {
         const uint32_t enc = sec_gates[j];
         const M2 gm = sec_gate(enc, theta, false);
@@ -260,9 +260,11 @@ cudaError_t launch_finalize(cudaStream_t st, int n_sec, const uint32_t *sec_q,
                             const uint32_t *sec_gates, const double *sec_gamma,
                             const double *theta, int n, const double *kout, double *grad,
                             const double *expect, uint32_t batch, double *loss) {
-    const int blocks = (n_sec + 127) / 128 + 1;
-    finalize_kernel<<<blocks, 128, 0, st>>>(n_sec, sec_q, sec_stage, sec_off, sec_gates, sec_gamma,
-                                            theta, n, kout, grad, expect, batch, loss);
+    loss_kernel<<<1, 32, 0, st>>>(expect, batch, loss);
+    if (n_sec > 0)
+        finalize_kernel<<<(n_sec + 127) / 128, 128, 0, st>>>(n_sec, sec_q, sec_stage, sec_off,
+                                                             sec_gates, sec_gamma, theta, n, kout,
+                                                             grad, loss);
     return cudaGetLastError();
 }
 

@@ -1,0 +1,44 @@
+// qfuse-b200 C++ drop-in for the reference's hot path.
+//
+// Same types and signatures as the reference engine (compile against the
+// reference headers, proj/include), executed on a B200 through the C-ABI in
+// include/qfuse_b200.h:
+//
+//   qfuse::b200::gradient          <- qfuse::gradient<float>         engine.hpp:139-142
+//   qfuse::b200::run_checkpointed  <- qfuse::run_checkpointed<float> checkpoint.hpp:65-69
+//   qfuse::b200::naive_gradient    <- qfuse::naive_gradient<float>   engine.hpp:146-149
+//
+// A caller switches by replacing `qfuse::gradient<float>(...)` with
+// `qfuse::b200::gradient(...)`. Errors are rethrown as the
+// reference's exception types: std::invalid_argument (C-ABI code 2),
+// qfuse::CapacityError (3), std::runtime_error (4).
+#pragma once
+
+#include <cstdint>
+#include <span>
+
+#include "qfuse/checkpoint.hpp"
+#include "qfuse/circuit.hpp"
+#include "qfuse/engine.hpp"
+#include "qfuse/fusion.hpp"
+#include "qfuse/statevec.hpp"
+
+namespace qfuse::b200 {
+
+// CUDA device used by the calls of this thread (default 0, or $QFUSE_B200_DEVICE).
+void set_device(int device);
+
+GradientResult gradient(const FusedCircuit &fused, const BatchedState<float> &psi0,
+                        std::span<const double> theta, const PauliString &pauli,
+                        StorageMode mode, MemoryAccountant *accountant = nullptr);
+
+GradientResult run_checkpointed(const FusedCircuit &fused, const BatchedState<float> &psi0,
+                                std::span<const double> theta, const PauliString &pauli,
+                                const CheckpointPlan &plan, StorageMode mode,
+                                MemoryAccountant *accountant = nullptr);
+
+GradientResult naive_gradient(const Circuit &circuit, const BatchedState<float> &psi0,
+                              std::span<const double> theta, const PauliString &pauli,
+                              MemoryAccountant *accountant = nullptr);
+
+} // namespace qfuse::b200

@@ -188,3 +188,19 @@ def test_device_random_state(ctx):
     plan.download_psi0_ptr(host.ctypes.data)
     want = C.new_random_state(n, 5 + batch, 1234)[5:]
     np.testing.assert_allclose(host, want, rtol=0, atol=2e-7)
+
+
+def test_cpp_dropin_shim():
+    """The reference's own C++ calling code (qfuse::gradient<float>,
+    run_checkpointed<float>, naive_gradient<float>) vs the qfuse::b200 drop-in
+    on the same BatchedState / FusedCircuit / PauliString objects."""
+    import os
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = os.path.join(root, "build", "tests", "shim_parity")
+    if not os.path.exists(exe):
+        pytest.skip("build/tests/shim_parity not built (needs the reference headers at build time)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "ALL PASSED" in r.stdout
