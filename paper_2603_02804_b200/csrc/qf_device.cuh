@@ -170,30 +170,43 @@ __device__ __forceinline__ float2 cmulc(float2 a, float2 b) { // conj(a) * b
     return make_float2(a.x * b.x + a.y * b.y, a.x * b.y - a.y * b.x);
 }
 
-// Ry(beta) = [[c, -s], [s, c]] (circuit.cpp:67-68) on register bit B;
-// cs = (c, c, s, s). Backward applies Ry(-beta).
+// Ry(beta) = [[c, -s], [s, c]] (circuit.cpp:67-68) on register bit B, with c
+// factored out: Ry = c [[1, -t], [t, 1]], t = s / c, so the bit costs ONE FFMA2
+// per output amplitude; the c of the group's four bits are re-applied together
+// (one FMUL2 per amplitude, ry_round). fp32 rounding of fma(-t, b, a) * c is
+// the same relative error as c a - s b; c is clamped at 2^-20 (beta ~ pi) so
+// intermediates stay < 2^80 x |amplitude| (error <= 1e-6 relative, only there).
+// rys entry: (t, t, c, 0). Backward applies Ry(-beta): t -> -t.
 template <int B, bool INV>
-__device__ __forceinline__ void ry2(float2 (&v)[16], float4 cs) {
-    const float2 C = make_float2(cs.x, cs.y);
-    const float2 S = INV ? make_float2(-cs.z, -cs.w) : make_float2(cs.z, cs.w);
-    const float2 N = make_float2(-S.x, -S.y);
+__device__ __forceinline__ void ry2(float2 (&v)[16], float4 e) {
+    const float2 K = make_float2(e.x, e.y);
+    const float2 N = make_float2(-e.x, -e.y);
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
         if (j & (1 << B)) continue;
         const float2 a = v[j], b = v[j | (1 << B)];
-        v[j] = f2fma(N, b, f2mul(C, a));
-        v[j | (1 << B)] = f2fma(S, a, f2mul(C, b));
+        v[j] = f2fma(INV ? K : N, b, a);             // a -/+ t b
+        v[j | (1 << B)] = f2fma(INV ? N : K, a, b);  // b +/- t a
     }
 }
-// One Ry round on the rotated bits of group G. FULL (all four bits rotated,
-// the HEA case) is branch-free so the register array never has to be merged
-// across control flow; otherwise warp-uniform branches per bit.
+// One Ry round on the rotated bits of group G, then the product of their m
+// (mg = (M, M)). FULL (all four bits rotated, the HEA case) has no per-bit
+// branches around the register array; otherwise warp-uniform branches.
 template <int G, bool INV, bool FULL>
-__device__ __forceinline__ void ry_round(float2 (&v)[16], const float4 *rys, uint32_t rot) {
+__device__ __forceinline__ void ry_round(float2 (&v)[16], const float4 *rys, uint32_t rot,
+                                         float2 mg) {
     if (FULL || (rot & (1u << (4 * G + 0)))) ry2<0, INV>(v, rys[4 * G + 0]);
     if (FULL || (rot & (1u << (4 * G + 1)))) ry2<1, INV>(v, rys[4 * G + 1]);
     if (FULL || (rot & (1u << (4 * G + 2)))) ry2<2, INV>(v, rys[4 * G + 2]);
     if (FULL || (rot & (1u << (4 * G + 3)))) ry2<3, INV>(v, rys[4 * G + 3]);
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = f2mul(mg, v[j]);
+}
+// (cos, sin) of beta/2 -> rys entry; the group scale is the product of m.
+__device__ __forceinline__ float4 ry_entry(float2 cs) {
+    const float c = fmaxf(cs.x, 0x1.0p-20f); // cos(beta/2) >= 0 (beta in [0, pi])
+    const float t = cs.y / c;
+    return make_float4(t, t, c, 0.f);
 }
 
 // K_ab = sum psi_a conj(lam_b) over the pairs of register bit B, written as
@@ -333,7 +346,8 @@ __device__ __forceinline__ void apply_diag(float2 (&v)[16], const DiagCtx &d, co
 
 // ---------------------------------------------------------- group phases
 struct PhaseEnv {
-    const float4 *rys; // smem [2][12] (c, c, s, s): round 0, round 1
+    const float4 *rys; // smem [2][12] ry_entry(): round 0, round 1
+    const float2 *mgs; // smem [2][3] group scales (M, M): round 0, round 1
     uint32_t rot;
     DiagCtx d;
     const float2 *treg_s;
@@ -345,9 +359,9 @@ template <int G, uint32_t OPS, bool FULL>
 __device__ __forceinline__ void phase_fwd(uint8_t *tile, uint32_t tau, const PhaseEnv &e) {
     float2 v[16];
     lds16<G>(tile, tau, v);
-    if (OPS & 1u) ry_round<G, false, FULL>(v, e.rys, e.rot);
+    if (OPS & 1u) ry_round<G, false, FULL>(v, e.rys, e.rot, e.mgs[G]);
     if (OPS & 2u) apply_diag<false>(v, e.d, e.treg_s);
-    if (OPS & 4u) ry_round<G, false, FULL>(v, e.rys + 12, e.rot);
+    if (OPS & 4u) ry_round<G, false, FULL>(v, e.rys + 12, e.rot, e.mgs[3 + G]);
     sts16<G>(tile, tau, v);
 }
 template <int G, uint32_t OPS, bool FULL>
@@ -356,8 +370,8 @@ __device__ __forceinline__ void phase_bwd(uint8_t *pt, uint8_t *lt, uint32_t tau
     lds16<G>(pt, tau, p);
     lds16<G>(lt, tau, l);
     if (OPS & 4u) {
-        ry_round<G, true, FULL>(p, e.rys + 12, e.rot);
-        ry_round<G, true, FULL>(l, e.rys + 12, e.rot);
+        ry_round<G, true, FULL>(p, e.rys + 12, e.rot, e.mgs[3 + G]);
+        ry_round<G, true, FULL>(l, e.rys + 12, e.rot, e.mgs[3 + G]);
         kmeasure<G, FULL>(p, l, e.rot, e.acc_w + 12 * 8);
     }
     if (OPS & 2u) {
@@ -365,8 +379,8 @@ __device__ __forceinline__ void phase_bwd(uint8_t *pt, uint8_t *lt, uint32_t tau
         apply_diag<true>(l, e.d, e.treg_s);
     }
     if (OPS & 1u) {
-        ry_round<G, true, FULL>(p, e.rys, e.rot);
-        ry_round<G, true, FULL>(l, e.rys, e.rot);
+        ry_round<G, true, FULL>(p, e.rys, e.rot, e.mgs[G]);
+        ry_round<G, true, FULL>(l, e.rys, e.rot, e.mgs[G]);
         kmeasure<G, FULL>(p, l, e.rot, e.acc_w);
     }
     sts16<G>(pt, tau, p);

@@ -24,7 +24,7 @@ constexpr size_t kAccBytes = size_t(8) * 2 * 12 * 8 * sizeof(double); // [warp][
 constexpr int nbuf(bool bwd) { return bwd ? 1 : 2; }
 constexpr size_t pass_smem(bool bwd) {
     return size_t(nbuf(bwd)) * kTileBytes * (bwd ? 2 : 1) + 64 /*mbar*/ + 24 * 16 /*rys*/ +
-           16 * 8 /*treg*/ + (bwd ? kAccBytes : 0) + 1024 /*align*/;
+           16 * 8 /*treg*/ + 8 * 8 /*mgs*/ + (bwd ? kAccBytes : 0) + 1024 /*align*/;
 }
 
 template <bool BWD>
@@ -40,20 +40,27 @@ __global__ void __launch_bounds__(kThreads, BWD ? 2 : 3)
     uint64_t *mbar = reinterpret_cast<uint64_t *>(tail);
     float4 *rys = reinterpret_cast<float4 *>(tail + 64);
     float2 *treg_s = reinterpret_cast<float2 *>(tail + 64 + 24 * 16);
-    double *acc = reinterpret_cast<double *>(tail + 64 + 24 * 16 + 16 * 8);
+    float2 *mgs = treg_s + 16; // [2 rounds][3 groups]
+    double *acc = reinterpret_cast<double *>(tail + 64 + 24 * 16 + 16 * 8 + 8 * 8);
     const uint32_t tid = threadIdx.x, warp = tid >> 5;
 
     if (tid < 24) {
         const int r = tid / 12, lb = tid % 12;
         const int s = r == 0 ? p.s0 : p.s1;
-        float4 v = make_float4(1.f, 1.f, 0.f, 0.f);
-        if (s >= 0 && ((p.rot_mask >> lb) & 1u)) {
-            const float2 cs = p.ry[size_t(s) * p.n + p.qmap[lb]];
-            v = make_float4(cs.x, cs.x, cs.y, cs.y);
-        }
+        float4 v = make_float4(0.f, 0.f, 1.f, 0.f); // identity: t = 0, m = 1
+        if (s >= 0 && ((p.rot_mask >> lb) & 1u)) v = ry_entry(p.ry[size_t(s) * p.n + p.qmap[lb]]);
         rys[tid] = v;
     } else if (tid < 40) {
         treg_s[tid - 24] = p.dt ? p.dt->treg[tid - 24] : make_float2(1.f, 0.f);
+    } else if (tid < 46) { // group scales: product of the factored m per (round, group)
+        const int r = (tid - 40) / 3, g = (tid - 40) % 3;
+        const int s = r == 0 ? p.s0 : p.s1;
+        float M = 1.f;
+        for (int b = 0; b < 4; ++b) {
+            const int lb = 4 * g + b;
+            if (s >= 0 && ((p.rot_mask >> lb) & 1u)) M *= ry_entry(p.ry[size_t(s) * p.n + p.qmap[lb]]).z;
+        }
+        mgs[tid - 40] = make_float2(M, M);
     }
     if (BWD) {
         for (uint32_t i = tid; i < kAccBytes / 8; i += kThreads) acc[i] = 0.0;
@@ -87,6 +94,7 @@ __global__ void __launch_bounds__(kThreads, BWD ? 2 : 3)
     }
     PhaseEnv env;
     env.rys = rys;
+    env.mgs = mgs;
     env.rot = p.rot_mask;
     env.treg_s = treg_s;
     env.acc_w = acc + warp * 2 * 12 * 8;

@@ -105,7 +105,7 @@ __global__ void __launch_bounds__(kThreads) seed_kernel(const SeedParams p) {
 constexpr size_t kResAcc = size_t(8) * 2 * 12 * 8 * sizeof(double);
 constexpr size_t res_smem() {
     return size_t(2) * kTileBytes + size_t(kTileAmps) * sizeof(double) + 64 +
-           2 * 24 * 16 /*rys*/ + 2 * 16 * 8 /*treg*/ + kResAcc + 1024;
+           2 * 24 * 16 /*rys*/ + 2 * 16 * 8 /*treg*/ + 2 * 6 * 8 /*mgs*/ + kResAcc + 1024;
 }
 
 __global__ void __launch_bounds__(kThreads, 2)
@@ -121,7 +121,8 @@ __global__ void __launch_bounds__(kThreads, 2)
     uint64_t *mbar = reinterpret_cast<uint64_t *>(tail);
     float4 *rys = reinterpret_cast<float4 *>(tail + 64);                  // [2 slots][24]
     float2 *treg_s = reinterpret_cast<float2 *>(tail + 64 + 2 * 24 * 16); // [2 slots][16]
-    double *acc = reinterpret_cast<double *>(tail + 64 + 2 * 24 * 16 + 2 * 16 * 8);
+    float2 *mgs = treg_s + 2 * 16;                                       // [2 slots][2][3]
+    double *acc = reinterpret_cast<double *>(tail + 64 + 2 * 24 * 16 + 2 * 16 * 8 + 2 * 6 * 8);
     const uint32_t tid = threadIdx.x, warp = tid >> 5;
     const int n = p.n, S = p.stages;
     const uint32_t rot = (n >= 12) ? 0xFFFu : ((1u << n) - 1u);
@@ -129,8 +130,10 @@ __global__ void __launch_bounds__(kThreads, 2)
     const int spt = kTileAmps >> (n < 12 ? n : 12);
 
     for (uint32_t i = tid; i < kResAcc / 8; i += kThreads) acc[i] = 0.0;
-    if (tid < 48) { // round-0 halves stay identity
-        rys[tid] = make_float4(1.f, 1.f, 0.f, 0.f);
+    if (tid < 48) { // round-0 halves stay identity (t = 0, m = 1)
+        rys[tid] = make_float4(0.f, 0.f, 1.f, 0.f);
+    } else if (tid < 60) {
+        mgs[tid - 48] = make_float2(1.f, 1.f);
     }
     if (tid == 0) {
         prefetch_map(&m_psi0);
@@ -144,20 +147,22 @@ __global__ void __launch_bounds__(kThreads, 2)
         const int sl = s & 1;
         if (tid >= 64 && tid < 76) {
             const int lb = tid - 64;
-            float4 v = make_float4(1.f, 1.f, 0.f, 0.f);
-            if (lb < n) {
-                const float2 cs = p.ry[size_t(s) * n + lb];
-                v = make_float4(cs.x, cs.x, cs.y, cs.y);
-            }
-            rys[sl * 24 + 12 + lb] = v;
+            rys[sl * 24 + 12 + lb] = lb < n ? ry_entry(p.ry[size_t(s) * n + lb]) : make_float4(0.f, 0.f, 1.f, 0.f);
         } else if (tid >= 76 && tid < 92) {
             treg_s[sl * 16 + (tid - 76)] = p.dt[s].treg[tid - 76];
+        } else if (tid >= 92 && tid < 95) { // round-1 group scales
+            const int g = tid - 92;
+            float M = 1.f;
+            for (int b = 0; b < 4; ++b)
+                if (4 * g + b < n) M *= ry_entry(p.ry[size_t(s) * n + 4 * g + b]).z;
+            mgs[sl * 6 + 3 + g] = make_float2(M, M);
         }
     };
     auto env_for = [&](int s) {
         PhaseEnv e;
         const int sl = s & 1;
         e.rys = rys + sl * 24;
+        e.mgs = mgs + sl * 6;
         e.rot = rot;
         e.treg_s = treg_s + sl * 16;
         e.acc_w = acc + warp * 2 * 12 * 8;
