@@ -287,12 +287,17 @@ Plan make_plan(const qf_gate *gates, size_t n_gates, uint32_t n, uint32_t n_para
                 if (g != L.gd && (L.rot_mask >> (4 * g)) & 0xFu) groups.push_back(g);
             auto add = [&](int g, uint8_t ops) { st.ph[st.nph++] = PassPhase{int8_t(g), ops}; };
             const uint8_t d_op = st.sd >= 0 ? 2 : 0;
-            if (st.s0 >= 0)
-                for (int g : groups) add(g, 1);
             const uint8_t gd_ops = uint8_t((st.s0 >= 0 ? 1 : 0) | d_op | (st.s1 >= 0 ? 4 : 0));
-            if (gd_ops) add(L.gd, gd_ops);
-            if (st.s1 >= 0)
-                for (int g : groups) add(g, 4);
+            if (gd_ops == 1) { // round 0 only: any order; keep a row group last (direct epilogue)
+                add(L.gd, 1);
+                for (int g : groups) add(g, 1);
+            } else {
+                if (st.s0 >= 0)
+                    for (int g : groups) add(g, 1);
+                if (gd_ops) add(L.gd, gd_ops);
+                if (st.s1 >= 0)
+                    for (int g : groups) add(g, 4);
+            }
             plan.steps.push_back(st);
             X = (X + 1) % NL;
         }
