@@ -14,7 +14,8 @@ import numpy as np
 from .circuits import GATE_DTYPE
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libqfuse_b200.so")
+# QFUSE_B200_LIB: alternative build of the same library (ablation experiments)
+LIB_PATH = os.environ.get("QFUSE_B200_LIB") or os.path.join(HERE, "libqfuse_b200.so")
 
 QF_OK, QF_EINVAL, QF_ECAPACITY, QF_EDEVICE = 0, 2, 3, 4
 

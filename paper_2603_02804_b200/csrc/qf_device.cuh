@@ -209,98 +209,74 @@ __device__ __forceinline__ float4 ry_entry(float2 cs) {
     return make_float4(t, t, c, 0.f);
 }
 
-// K_ab = sum psi_a conj(lam_b) over the pairs of register bit B, written as
-// 8 floats (K00, K01, K10, K11 as re, im). With ps = swap(psi):
-// Re = (psi (.) lam).x + .y,  Im = (ps (.) lam).x - .y.
-// K11 is not accumulated: tr K = sum_x psi_x conj(lam_x) = 2 sum_s E_s is the
-// same at every circuit point (psi and lambda evolve by the same unitary), so
-// the finalize kernel uses K11 = 2 loss - K00. 6 FFMA2 per pair instead of 8.
+// Gradient data of register bit B. Every reference gradient of the qubit's
+// section is (1/2) sum_m R_m Im Tr(sigma_m K) with K = sum psi lam^dag (the
+// generators only ever appear conjugated by unitaries, finalize_kernel), so
+// three real numbers per (stage, qubit) suffice:
+//   X = Im(K01 + K10),  Y = Re(K01 - K10),  Z = Im(K00 - K11).
+// With ps = swap(psi): (ps (.) lam).x - .y = Im(psi conj lam) and
+// (psi (.) lam).x + .y = Re(psi conj lam). 6 FFMA2 per pair; two interleaved
+// accumulator sets for ILP.
 template <int B>
-__device__ __forceinline__ void kbit(const float2 (&p)[16], const float2 (&ps)[16],
-                                     const float2 (&l)[16], float *k) {
-    float2 a00 = make_float2(0.f, 0.f), b00 = a00, a01 = a00, b01 = a00, a10 = a00, b10 = a00;
+__device__ __forceinline__ void kbit3(const float2 (&p)[16], const float2 (&ps)[16],
+                                      const float2 (&l)[16], float *out) {
+    float2 bx[2], ay[2], bz[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) bx[h] = ay[h] = bz[h] = make_float2(0.f, 0.f);
+    int pair = 0;
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
         if (j & (1 << B)) continue;
-        const int j1 = j | (1 << B);
-        a00 = f2fma(p[j], l[j], a00);
-        b00 = f2fma(ps[j], l[j], b00);
-        a01 = f2fma(p[j], l[j1], a01);
-        b01 = f2fma(ps[j], l[j1], b01);
-        a10 = f2fma(p[j1], l[j], a10);
-        b10 = f2fma(ps[j1], l[j], b10);
+        const int j1 = j | (1 << B), h = pair++ & 1;
+        const float2 nps1 = make_float2(-ps[j1].x, -ps[j1].y);
+        const float2 np1 = make_float2(-p[j1].x, -p[j1].y);
+        bz[h] = f2fma(ps[j], l[j], bz[h]);
+        bz[h] = f2fma(nps1, l[j1], bz[h]);
+        bx[h] = f2fma(ps[j], l[j1], bx[h]);
+        bx[h] = f2fma(ps[j1], l[j], bx[h]);
+        ay[h] = f2fma(p[j], l[j1], ay[h]);
+        ay[h] = f2fma(np1, l[j], ay[h]);
     }
-    k[0] = a00.x + a00.y;
-    k[1] = b00.x - b00.y;
-    k[2] = a01.x + a01.y;
-    k[3] = b01.x - b01.y;
-    k[4] = a10.x + a10.y;
-    k[5] = b10.x - b10.y;
-    k[6] = 0.f;
-    k[7] = 0.f;
+    out[0] = (bx[0].x + bx[1].x) - (bx[0].y + bx[1].y);
+    out[1] = (ay[0].x + ay[1].x) + (ay[0].y + ay[1].y);
+    out[2] = (bz[0].x + bz[1].x) - (bz[0].y + bz[1].y);
 }
 
-// Reduce-scatter of 32 per-lane values: afterwards lane L holds the warp sum
-// of value L (31 shuffles).
-__device__ __forceinline__ float warp_reduce_scatter32(float (&v)[32]) {
-    const uint32_t lane = threadIdx.x & 31u;
-#pragma unroll
-    for (int m = 16; m >= 1; m >>= 1) {
-        const bool up = (lane & m) != 0;
-#pragma unroll
-        for (int i = 0; i < m; ++i) {
-            const float send = up ? v[i] : v[i + m];
-            const float keep = up ? v[i + m] : v[i];
-            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, m);
-        }
-    }
-    return v[0];
-}
-
-// Reduce 8 per-lane values over the warp: lane L ends with the sum of value
-// L & 7 (7 + 2 shuffles).
-__device__ __forceinline__ float warp_reduce8(float (&v)[8]) {
-    const uint32_t lane = threadIdx.x & 31u;
-#pragma unroll
-    for (int m = 4; m >= 1; m >>= 1) {
-        const bool up = (lane & m) != 0;
-#pragma unroll
-        for (int i = 0; i < m; ++i) {
-            const float send = up ? v[i] : v[i + m];
-            const float keep = up ? v[i + m] : v[i];
-            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, m);
-        }
-    }
-    float r = v[0];
-    r += __shfl_xor_sync(0xffffffffu, r, 8);
-    r += __shfl_xor_sync(0xffffffffu, r, 16);
-    return r;
-}
-
-template <int G, int B, bool FULL>
-__device__ __forceinline__ void kmeasure_bit(const float2 (&p)[16], const float2 (&ps)[16],
-                                             const float2 (&l)[16], uint32_t rot, double *acc_w) {
-    if (!FULL && !(rot & (1u << (4 * G + B)))) return;
-    float k[8];
-    kbit<B>(p, ps, l, k);
-    const float r = warp_reduce8(k);
-    const uint32_t lane = threadIdx.x & 31u;
-    if (lane < 8) acc_w[(4 * G + B) * 8 + lane] += double(r);
-}
-
-// K of every rotated bit of group G at the current point, added (fp64) to
-// this warp's accumulator acc_w[local bit][8]; one bit at a time keeps the
-// live accumulators at 8.
+// (X, Y, Z) of the rotated bits of group G at the current point: 12 values
+// reduced over the warp in one 16-wide reduce-scatter (16 shuffles), then
+// added in fp64 to this warp's accumulator acc_w[local bit][8] (slots 0..2).
 template <int G, bool FULL>
 __device__ __forceinline__ void kmeasure(const float2 (&p)[16], const float2 (&l)[16],
                                          uint32_t rot, double *acc_w) {
+#if QF_ABLATE_K
+    return; // timing ablation only
+#endif
     float2 ps[16];
 #pragma unroll
     for (int j = 0; j < 16; ++j) ps[j] = make_float2(p[j].y, p[j].x);
-    kmeasure_bit<G, 0, FULL>(p, ps, l, rot, acc_w);
-    kmeasure_bit<G, 1, FULL>(p, ps, l, rot, acc_w);
-    kmeasure_bit<G, 2, FULL>(p, ps, l, rot, acc_w);
-    kmeasure_bit<G, 3, FULL>(p, ps, l, rot, acc_w);
+    float v[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = 0.f;
+    if (FULL || (rot & (1u << (4 * G + 0)))) kbit3<0>(p, ps, l, v + 0);
+    if (FULL || (rot & (1u << (4 * G + 1)))) kbit3<1>(p, ps, l, v + 3);
+    if (FULL || (rot & (1u << (4 * G + 2)))) kbit3<2>(p, ps, l, v + 6);
+    if (FULL || (rot & (1u << (4 * G + 3)))) kbit3<3>(p, ps, l, v + 9);
+    const uint32_t lane = threadIdx.x & 31u;
+#pragma unroll
+    for (int m = 8; m >= 1; m >>= 1) {
+        const bool up = (lane & m) != 0;
+#pragma unroll
+        for (int i = 0; i < m; ++i) {
+            const float send = up ? v[i] : v[i + m];
+            const float keep = up ? v[i + m] : v[i];
+            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, m);
+        }
+    }
+    const float r = v[0] + __shfl_xor_sync(0xffffffffu, v[0], 16);
+    if (lane < 12) {
+        const uint32_t bit = lane / 3u, comp = lane % 3u;
+        if (rot & (1u << (4 * G + bit))) acc_w[(4 * G + bit) * 8 + comp] += double(r);
+    }
 }
 
 // ------------------------------------------------------------- diagonal

@@ -9,6 +9,8 @@
 // costs ONE pass (the diagonal commutes with everything but the Ry's of its
 // own stage boundary). Backward passes undo the same ops on psi and lambda
 // and accumulate K = sum psi lambda^dag per (stage, qubit) in fp64.
+#include <cstdlib>
+
 #include "qf_device.cuh"
 
 namespace qfb {
@@ -19,23 +21,24 @@ using namespace dev;
 constexpr size_t kAccBytes = size_t(8) * 2 * 12 * 8 * sizeof(double); // [warp][round][bit][8]
 
 // Forward: 3 CTAs/SM, each double-buffered (load of tile i+1 overlaps tile i).
-// Backward: 2 CTAs/SM, single-buffered (psi + lambda = 64 KiB); the two CTAs
-// overlap each other's TMA traffic with compute.
-constexpr int nbuf(bool bwd) { return bwd ? 1 : 2; }
-constexpr size_t pass_smem(bool bwd) {
-    return size_t(nbuf(bwd)) * kTileBytes * (bwd ? 2 : 1) + 64 /*mbar*/ + 24 * 16 /*rys*/ +
+// Backward, NB = 1: 2 CTAs/SM, single-buffered (psi + lambda = 64 KiB); the two
+// CTAs overlap each other's TMA traffic with compute. NB = 3: 1 CTA/SM with a
+// 3-deep ring (load i+1 and store i-1 overlap tile i). Selected at plan time
+// (QF_BWD_PIPE=3 for the ring).
+constexpr size_t pass_smem(bool bwd, int nb) {
+    return size_t(nb) * kTileBytes * (bwd ? 2 : 1) + 64 /*mbar*/ + 24 * 16 /*rys*/ +
            16 * 8 /*treg*/ + 8 * 8 /*mgs*/ + (bwd ? kAccBytes : 0) + 1024 /*align*/;
 }
+constexpr int min_blocks(bool bwd, int nb) { return bwd ? (nb == 1 ? 2 : 1) : 3; }
 
-template <bool BWD>
-__global__ void __launch_bounds__(kThreads, BWD ? 2 : 3)
+template <bool BWD, int NB>
+__global__ void __launch_bounds__(kThreads, min_blocks(BWD, NB))
     pass_kernel(const __grid_constant__ PassParams p, const __grid_constant__ CUtensorMap m_in,
                 const __grid_constant__ CUtensorMap m_out,
                 const __grid_constant__ CUtensorMap m_lam) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = align1024(smem_raw);
     constexpr uint32_t kBuf = uint32_t(kTileBytes) * (BWD ? 2 : 1);
-    constexpr int NB = nbuf(BWD);
     uint8_t *tail = smem + NB * kBuf;
     uint64_t *mbar = reinterpret_cast<uint64_t *>(tail);
     float4 *rys = reinterpret_cast<float4 *>(tail + 64);
@@ -71,8 +74,7 @@ __global__ void __launch_bounds__(kThreads, BWD ? 2 : 3)
         prefetch_map(&m_in);
         prefetch_map(&m_out);
         if (BWD) prefetch_map(&m_lam);
-        mbar_init(&mbar[0], 1);
-        mbar_init(&mbar[1], 1);
+        for (int b = 0; b < NB; ++b) mbar_init(&mbar[b], 1);
         fence_mbar_init();
     }
     __syncthreads();
@@ -102,7 +104,7 @@ __global__ void __launch_bounds__(kThreads, BWD ? 2 : 3)
     env.d.sgn = 0;
     int it = 0;
     for (int t = blockIdx.x; t < p.tiles; t += stride, ++it) {
-        const int b = NB == 1 ? 0 : (it & 1);
+        const int b = it % NB;
         if (p.dt) env.d = diag_ctx(tid, tthr, thrinfo, p.dt, p.cz, p.tileinfo, uint32_t(t) & tis_mask);
         mbar_wait(&mbar[b], (it / NB) & 1);
         uint8_t *pt = smem + b * kBuf;
@@ -148,29 +150,42 @@ __global__ void __launch_bounds__(kThreads, BWD ? 2 : 3)
     }
 }
 
+int bwd_pipe() {
+    static int nb = [] {
+        const char *e = getenv("QF_BWD_PIPE");
+        return (e && atoi(e) == 3) ? 3 : 1;
+    }();
+    return nb;
+}
+
 bool g_attrs = false;
 cudaError_t ensure_attrs() {
     if (g_attrs) return cudaSuccess;
-    cudaError_t e = cudaFuncSetAttribute(pass_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int(pass_smem(false)));
+    cudaError_t e = cudaFuncSetAttribute(pass_kernel<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(pass_smem(false, 2)));
     if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(pass_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 int(pass_smem(true)));
+        e = cudaFuncSetAttribute(pass_kernel<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(pass_smem(true, 1)));
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(pass_kernel<true, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(pass_smem(true, 3)));
     g_attrs = e == cudaSuccess;
     return e;
 }
 
 } // namespace
 
-size_t pass_smem_bytes(bool backward) { return pass_smem(backward); }
+size_t pass_smem_bytes(bool backward) { return backward ? pass_smem(true, bwd_pipe()) : pass_smem(false, 2); }
 
 int pass_occupancy(bool backward) {
     if (ensure_attrs() != cudaSuccess) return 0;
     int blocks = 0;
-    if (backward)
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, pass_kernel<true>, kThreads, pass_smem(true));
+    if (!backward)
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, pass_kernel<false, 2>, kThreads, pass_smem(false, 2));
+    else if (bwd_pipe() == 3)
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, pass_kernel<true, 3>, kThreads, pass_smem(true, 3));
     else
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, pass_kernel<false>, kThreads, pass_smem(false));
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, pass_kernel<true, 1>, kThreads, pass_smem(true, 1));
     return blocks;
 }
 
@@ -180,10 +195,12 @@ cudaError_t launch_pass(cudaStream_t st, bool backward, int grid, const PassPara
     cudaError_t e = ensure_attrs();
     if (e != cudaSuccess) return e;
     const CUtensorMap &l = lam ? *lam : *psi_out;
-    if (backward)
-        pass_kernel<true><<<grid, kThreads, pass_smem(true), st>>>(p, *psi_in, *psi_out, l);
+    if (!backward)
+        pass_kernel<false, 2><<<grid, kThreads, pass_smem(false, 2), st>>>(p, *psi_in, *psi_out, l);
+    else if (bwd_pipe() == 3)
+        pass_kernel<true, 3><<<grid, kThreads, pass_smem(true, 3), st>>>(p, *psi_in, *psi_out, l);
     else
-        pass_kernel<false><<<grid, kThreads, pass_smem(false), st>>>(p, *psi_in, *psi_out, l);
+        pass_kernel<true, 1><<<grid, kThreads, pass_smem(true, 1), st>>>(p, *psi_in, *psi_out, l);
     return cudaGetLastError();
 }
 

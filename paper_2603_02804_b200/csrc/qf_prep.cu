@@ -150,8 +150,8 @@ __global__ void loss_kernel(const double *expect, uint32_t batch, double *loss) 
 
 // One thread per section: K at the point before Ry(beta) -> K at the run
 // start (Rz(gamma)^dag), then walk the run's gates: grad = Re Tr(dg K g^dag),
-// K <- g K g^dag. K11 = tr K - K00 with tr K = sum psi conj(lam) = 2 loss
-// (invariant along the circuit; the pass kernels do not accumulate it).
+// K <- g K g^dag. Only the traceless anti-Hermitian part of K (X, Y, Z from
+// the pass kernels) enters Re Tr(dg K g^dag), so K is rebuilt from it.
 __global__ void finalize_kernel(int n_sec, const uint32_t *sec_q, const uint32_t *sec_stage,
                                 const uint32_t *sec_off, const uint32_t *sec_gates,
                                 const double *sec_gamma, const double *theta, int n,
@@ -161,9 +161,12 @@ __global__ void finalize_kernel(int n_sec, const uint32_t *sec_q, const uint32_t
     const double *k = kout + (size_t(sec_stage[i]) * n + sec_q[i]) * 8;
     const double g = sec_gamma[i];
     const double2 e = make_double2(cos(g), sin(g));
-    const double tr = 2.0 * (*loss);
-    M2 K{{k[0], k[1]}, zmul(make_double2(k[2], k[3]), e), zmul(make_double2(k[4], k[5]), zconj(e)),
-         {tr - k[0], -k[1]}};
+    // K~ = (i/2)(X sx + Y sy + Z sz) carries exactly the Im Tr(sigma_m K) the
+    // gradients depend on (qf_device.cuh kbit3): [[iZ, Y + iX], [-Y + iX, -iZ]] / 2.
+    const double X = k[0], Y = k[1], Z = k[2];
+    (void)loss;
+    M2 K{{0.0, 0.5 * Z}, zmul(make_double2(0.5 * Y, 0.5 * X), e),
+         zmul(make_double2(-0.5 * Y, 0.5 * X), zconj(e)), {0.0, -0.5 * Z}};
     for (uint32_t j = sec_off[i]; j < sec_off[i + 1]; ++j) {
         const uint32_t enc = sec_gates[j];
         const M2 gm = sec_gate(enc, theta, false);
