@@ -132,6 +132,15 @@ def reference_sample(ref, n, layers_total, threads, budget_s=12.0):
     return sps, sample, (layers, batch, dt)
 
 
+def host_threads():
+    """All host cores this process may use (torchrun exports OMP_NUM_THREADS=1,
+    which must not throttle the reference's OpenMP arm)."""
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -140,7 +149,7 @@ def run_reference(args):
     from oracles import RefLib
     wl = WORKLOADS[args.workload]
     ref = RefLib()
-    threads = ref.max_threads()
+    threads = host_threads()
     vals = []
     sample = None
     for i in range(args.warmup + args.steps):
@@ -189,9 +198,14 @@ def run_ours(args):
     if world != args.gpus:
         log(f"note: WORLD_SIZE={world} but --gpus={args.gpus}; using WORLD_SIZE")
         args.gpus = world
-    torch.cuda.set_device(local)
+    dev = local % max(1, torch.cuda.device_count())  # tolerate fewer GPUs than ranks (tests)
+    torch.cuda.set_device(dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("QF_DIST_BACKEND", "nccl")  # gloo: single-GPU test of this path
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group(backend)
     wl = dict(WORKLOADS[args.workload])
     if args.batch:
         wl["batch"] = args.batch
@@ -202,7 +216,7 @@ def run_ours(args):
     n, layers, B = wl["n"], wl["layers"], wl["batch"]
     gates, M = C.build_hea(n, layers)
     pauli = C.parse_pauli(C.repeated_ixyz_label(n))
-    ctx = pkg.Context(local)
+    ctx = pkg.Context(dev)
     plan = pkg.Plan(ctx, gates, n, M, layers, wl["ckpt"], B, pauli)
     plan.random_psi0(SEED_STATE, first_sample=rank * B)
     theta_h = torch.from_numpy(C.random_parameters(M, SEED_THETA)).pin_memory()
@@ -222,7 +236,7 @@ def run_ours(args):
     plan.set_profiling(True)
     plan.profile(reset=True)
 
-    sampler = ClockSampler(local) if rank == 0 else None
+    sampler = ClockSampler(dev) if rank == 0 else None
     barrier()
     torch.cuda.synchronize()
     if sampler:
@@ -303,6 +317,21 @@ def run_ours(args):
     S = (1 << n) * 8
     bu = S * (6 * P * layers + layers / k + 1) * B
     roofline["step_formula_frac"] = bu / (ms_per_step / 1e3) / (peak * 1e9)
+    roofline["step_formula"] = f"B_U = S(6Pd + d/k + 1) with P={P} (BASELINE.md §2), our schedule moves P=1"
+    # FP32 (CUDA-core) roofline of the dominant kernel: the paired-pass kernels are
+    # FP32-bound. Algorithmic lane-FMA per amplitude per stage:
+    # forward 2n (one FFMA2 per output per qubit) + n/2 (group scales) + 8 (diag);
+    # backward 4n (Ry on psi and lambda) + 6n (X, Y, Z) + n (scales) + 16 (diag).
+    fp = os.path.join(ROOT, "profiles", "fp32_peak.json")
+    fp32_peak = json.load(open(fp))["tfma_per_s"] if os.path.exists(fp) else 36.9
+    per_amp = {"backward_pass": 11 * n + 16, "forward_pass": 2.5 * n + 8}.get(dom)
+    if per_amp and n > 12:
+        stages_per_launch = layers / max(1, d["launches"] / max(1, args.steps))
+        lane_fma = per_amp * B * (1 << n) * stages_per_launch
+        ach = lane_fma / (d["ms"] / d["launches"] / 1e3) / 1e12
+        roofline["fp32"] = {"achieved": ach, "peak": fp32_peak, "unit": "TFMA/s",
+                            "frac": ach / fp32_peak, "lane_fma_per_amp_stage": per_amp,
+                            "peak_source": "tools/ffma_probe.cu on this pool (profiles/fp32_peak.json)"}
 
     line = {
         "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world,
@@ -318,7 +347,7 @@ def run_ours(args):
             sys.path.insert(0, os.path.join(ROOT, "tests"))
             from oracles import RefLib
             ref = RefLib()
-            th = ref.max_threads()
+            th = host_threads()
             sps, sample, _ = reference_sample(ref, n, layers, th)
             line["cpu_baseline"] = {"value": sps, "unit": "samples/s", "cores": th,
                                     "kind": "reference", "sample": sample}
