@@ -241,9 +241,9 @@ __global__ void __launch_bounds__(kThreads, 2)
             }
             __syncthreads();
         }
-        if (tid < uint32_t(spt)) {
-            const uint64_t sample = uint64_t(t) * spt + tid;
-            if (sample < p.batch) p.expect[sample] = es[tid << (n < 12 ? n : 12)];
+        for (uint32_t ls = tid; ls < uint32_t(spt); ls += kThreads) { // n < 4: > 256 samples/tile
+            const uint64_t sample = uint64_t(t) * spt + ls;
+            if (sample < p.batch) p.expect[sample] = es[ls << (n < 12 ? n : 12)];
         }
         // ---------------- backward
         if (S > 0) load_stage(S - 1);

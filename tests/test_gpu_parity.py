@@ -204,3 +204,86 @@ def test_cpp_dropin_shim():
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "ALL PASSED" in r.stdout
+
+
+def _one(ctx, gates, n, npar, psi0, theta, label, layers=0):
+    pauli = C.parse_pauli(label)
+    return capi.gradient_c64(ctx, gates, n, npar, layers, 0, psi0, theta, pauli)
+
+
+def test_known_answer_single_rx(ctx):
+    """Single Rx(0.3) on |0>, O = Z: loss cos 0.3, grad -sin 0.3
+    (test_engine.cpp:284-302)."""
+    g = np.zeros(1, C.GATE_DTYPE)
+    g[0] = (C.ROT, C.X, 0, 0, 0, 0)
+    psi0 = np.zeros((1, 2, 2), np.float32)
+    psi0[0, 0, 0] = 1.0
+    res = _one(ctx, g, 1, 1, psi0, np.array([0.3]), "Z")
+    assert abs(res.loss - np.cos(0.3)) < 1e-6
+    assert abs(res.gradient[0] + np.sin(0.3)) < 1e-6
+
+
+def test_stationary_point_theta_zero(ctx):
+    """theta = 0 on |000> with ZZZ: loss 1, all gradients 0 (test_engine.cpp:395-405)."""
+    gates, npar = C.build_hea(3, 2)
+    psi0 = np.zeros((2, 8, 2), np.float32)
+    psi0[:, 0, 0] = 1.0
+    res = _one(ctx, gates, 3, npar, psi0, np.zeros(npar), "ZZZ")
+    assert abs(res.loss - 2.0) < 1e-6
+    assert np.max(np.abs(res.gradient)) < 1e-6
+
+
+def test_rx_pi_flips(ctx, oracle):
+    """Rx(pi) on qubit 0 of |00> -> -i|01>: <Z on q0> = -1 (test_engine.cpp:80-92)."""
+    g = np.zeros(1, C.GATE_DTYPE)
+    g[0] = (C.ROT, C.X, 0, 0, 0, 0)
+    psi0 = np.zeros((1, 4, 2), np.float32)
+    psi0[0, 0, 0] = 1.0
+    res = _one(ctx, g, 2, 1, psi0, np.array([np.pi]), "IZ")
+    assert abs(res.loss + 1.0) < 1e-6
+
+
+def test_no_parameters_and_cz_only(ctx, oracle):
+    """A circuit with no rotations (only CZ) still yields the expectation."""
+    g = np.zeros(3, C.GATE_DTYPE)
+    for i, (a, b) in enumerate([(0, 1), (1, 2), (0, 2)]):
+        g[i] = (C.CZ, 0, 0, a, b, 0)
+    psi0 = C.new_random_state(3, 4, 5)
+    res = _one(ctx, g, 3, 0, psi0, np.zeros(0), "XYZ")
+    loss, _, exp = oracle.gradient(g, 3, 0, psi0, np.zeros(0), C.parse_pauli("XYZ"))
+    assert abs(res.loss - loss) < 1e-5 and rel_diff(res.expect, exp) < 1e-4
+
+
+@pytest.mark.parametrize("n,batch", [(3, 1), (3, 513), (5, 130), (12, 3), (14, 5)])
+def test_ragged_batches(ctx, oracle, n, batch):
+    """Batches that do not fill the last 4096-amplitude tile (TMA OOB path)."""
+    gates, npar, theta, psi0, pauli = _hea_case(n, 2, batch, seed=31)
+    res = capi.gradient_c64(ctx, gates, n, npar, 2, 0, psi0, theta, pauli)
+    _check(res, oracle.gradient(gates, n, npar, psi0, theta, pauli))
+
+
+def test_device_psi0_and_device_outputs(ctx, oracle):
+    """qf_plan_set_psi0_device + qf_plan_gradient_device (the data-parallel path)."""
+    torch = pytest.importorskip("torch")
+    n, layers, batch = 13, 2, 3
+    gates, npar, theta, psi0, pauli = _hea_case(n, layers, batch, seed=12)
+    plan = capi.Plan(ctx, gates, n, npar, layers, 0, batch, pauli)
+    d_psi = torch.from_numpy(psi0).cuda()
+    d_theta = torch.from_numpy(theta).cuda()
+    out = torch.empty(npar + 1 + batch, dtype=torch.float64, device="cuda")
+    plan.set_psi0_device(d_psi.data_ptr())
+    plan.gradient_device(d_theta.data_ptr(), out.data_ptr())
+    plan.synchronize()
+    o = out.cpu().numpy()
+    loss, grad, exp = oracle.gradient(gates, n, npar, psi0, theta, pauli)
+    assert rel_diff(o[:npar], grad) <= TOL
+    assert abs(o[npar] - loss) <= TOL * max(1.0, float(np.sum(np.abs(exp))))
+    assert rel_diff(o[npar + 1:], exp) <= TOL
+
+
+def test_deep_circuit_uncompute_drift(ctx, oracle):
+    """200 layers of uncompute with re-anchoring every 10: fp32 stays within tolerance."""
+    n, layers = 13, 200
+    gates, npar, theta, psi0, pauli = _hea_case(n, layers, 1, seed=77)
+    res = capi.gradient_c64(ctx, gates, n, npar, layers, 10, psi0, theta, pauli)
+    _check(res, oracle.gradient(gates, n, npar, psi0, theta, pauli))
