@@ -190,17 +190,21 @@ __device__ __forceinline__ void ry2(float2 (&v)[16], float4 e) {
     }
 }
 // One Ry round on the rotated bits of group G, then the product of their m
-// (mg = (M, M)). FULL (all four bits rotated, the HEA case) has no per-bit
-// branches around the register array; otherwise warp-uniform branches.
+// (mg = (M, M)) unless the pass folds every scale of its two rounds into its
+// diagonal (scale == false, pass_prologue). FULL (all four bits rotated, the
+// HEA case) has no per-bit branches around the register array; otherwise
+// warp-uniform branches.
 template <int G, bool INV, bool FULL>
 __device__ __forceinline__ void ry_round(float2 (&v)[16], const float4 *rys, uint32_t rot,
-                                         float2 mg) {
+                                         float2 mg, bool scale) {
     if (FULL || (rot & (1u << (4 * G + 0)))) ry2<0, INV>(v, rys[4 * G + 0]);
     if (FULL || (rot & (1u << (4 * G + 1)))) ry2<1, INV>(v, rys[4 * G + 1]);
     if (FULL || (rot & (1u << (4 * G + 2)))) ry2<2, INV>(v, rys[4 * G + 2]);
     if (FULL || (rot & (1u << (4 * G + 3)))) ry2<3, INV>(v, rys[4 * G + 3]);
+    if (scale) {
 #pragma unroll
-    for (int j = 0; j < 16; ++j) v[j] = f2mul(mg, v[j]);
+        for (int j = 0; j < 16; ++j) v[j] = f2mul(mg, v[j]);
+    }
 }
 // (cos, sin) of beta/2 -> rys entry; the group scale is the product of m.
 __device__ __forceinline__ float4 ry_entry(float2 cs) {
@@ -214,53 +218,48 @@ __device__ __forceinline__ float4 ry_entry(float2 cs) {
 // generators only ever appear conjugated by unitaries, finalize_kernel), so
 // three real numbers per (stage, qubit) suffice:
 //   X = Im(K01 + K10),  Y = Re(K01 - K10),  Z = Im(K00 - K11).
-// With ps = swap(psi): (ps (.) lam).x - .y = Im(psi conj lam) and
-// (psi (.) lam).x + .y = Re(psi conj lam). 6 FFMA2 per pair; two interleaved
-// accumulator sets for ILP.
+// With ps = swap(psi) (a free operand swizzle of FFMA2):
+// (ps (.) lam).x - .y = Im(psi conj lam), (psi (.) lam).x + .y = Re(psi conj lam).
+// 6 FFMA2 per pair into ONE accumulator per output (measured 29 vs 24 TFMA/s
+// for two interleaved sets, tools/ffma2_patterns.cu); the four bits of a
+// group give 12 independent chains.
 template <int B>
-__device__ __forceinline__ void kbit3(const float2 (&p)[16], const float2 (&ps)[16],
-                                      const float2 (&l)[16], float *out) {
-    float2 bx[2], ay[2], bz[2];
-#pragma unroll
-    for (int h = 0; h < 2; ++h) bx[h] = ay[h] = bz[h] = make_float2(0.f, 0.f);
-    int pair = 0;
+__device__ __forceinline__ void kbit3(const float2 (&p)[16], const float2 (&l)[16], float *out) {
+    float2 bx = make_float2(0.f, 0.f), ay = bx, bz = bx;
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
         if (j & (1 << B)) continue;
-        const int j1 = j | (1 << B), h = pair++ & 1;
-        const float2 nps1 = make_float2(-ps[j1].x, -ps[j1].y);
-        const float2 np1 = make_float2(-p[j1].x, -p[j1].y);
-        bz[h] = f2fma(ps[j], l[j], bz[h]);
-        bz[h] = f2fma(nps1, l[j1], bz[h]);
-        bx[h] = f2fma(ps[j], l[j1], bx[h]);
-        bx[h] = f2fma(ps[j1], l[j], bx[h]);
-        ay[h] = f2fma(p[j], l[j1], ay[h]);
-        ay[h] = f2fma(np1, l[j], ay[h]);
+        const int j1 = j | (1 << B);
+        const float2 ps0 = make_float2(p[j].y, p[j].x), ps1 = make_float2(p[j1].y, p[j1].x);
+        bz = f2fma(ps0, l[j], bz);
+        bx = f2fma(ps0, l[j1], bx);
+        ay = f2fma(p[j], l[j1], ay);
+        ay = f2fma(make_float2(-p[j1].x, -p[j1].y), l[j], ay);
+        bx = f2fma(ps1, l[j], bx);
+        bz = f2fma(make_float2(-ps1.x, -ps1.y), l[j1], bz);
     }
-    out[0] = (bx[0].x + bx[1].x) - (bx[0].y + bx[1].y);
-    out[1] = (ay[0].x + ay[1].x) + (ay[0].y + ay[1].y);
-    out[2] = (bz[0].x + bz[1].x) - (bz[0].y + bz[1].y);
+    out[0] = bx.x - bx.y;
+    out[1] = ay.x + ay.y;
+    out[2] = bz.x - bz.y;
 }
 
 // (X, Y, Z) of the rotated bits of group G at the current point: 12 values
 // reduced over the warp in one 16-wide reduce-scatter (16 shuffles), then
-// added in fp64 to this warp's accumulator acc_w[local bit][8] (slots 0..2).
+// added in fp64 (times kc, the pass's scale correction) to this warp's
+// accumulator acc_w[local bit][8] (slots 0..2).
 template <int G, bool FULL>
 __device__ __forceinline__ void kmeasure(const float2 (&p)[16], const float2 (&l)[16],
-                                         uint32_t rot, double *acc_w) {
+                                         uint32_t rot, double *acc_w, float kc) {
 #if QF_ABLATE_K
     return; // timing ablation only
 #endif
-    float2 ps[16];
-#pragma unroll
-    for (int j = 0; j < 16; ++j) ps[j] = make_float2(p[j].y, p[j].x);
     float v[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) v[i] = 0.f;
-    if (FULL || (rot & (1u << (4 * G + 0)))) kbit3<0>(p, ps, l, v + 0);
-    if (FULL || (rot & (1u << (4 * G + 1)))) kbit3<1>(p, ps, l, v + 3);
-    if (FULL || (rot & (1u << (4 * G + 2)))) kbit3<2>(p, ps, l, v + 6);
-    if (FULL || (rot & (1u << (4 * G + 3)))) kbit3<3>(p, ps, l, v + 9);
+    if (FULL || (rot & (1u << (4 * G + 0)))) kbit3<0>(p, l, v + 0);
+    if (FULL || (rot & (1u << (4 * G + 1)))) kbit3<1>(p, l, v + 3);
+    if (FULL || (rot & (1u << (4 * G + 2)))) kbit3<2>(p, l, v + 6);
+    if (FULL || (rot & (1u << (4 * G + 3)))) kbit3<3>(p, l, v + 9);
     const uint32_t lane = threadIdx.x & 31u;
 #pragma unroll
     for (int m = 8; m >= 1; m >>= 1) {
@@ -275,7 +274,7 @@ __device__ __forceinline__ void kmeasure(const float2 (&p)[16], const float2 (&l
     const float r = v[0] + __shfl_xor_sync(0xffffffffu, v[0], 16);
     if (lane < 12) {
         const uint32_t bit = lane / 3u, comp = lane % 3u;
-        if (rot & (1u << (4 * G + bit))) acc_w[(4 * G + bit) * 8 + comp] += double(r);
+        if (rot & (1u << (4 * G + bit))) acc_w[(4 * G + bit) * 8 + comp] += double(r) * double(kc);
     }
 }
 
@@ -325,19 +324,24 @@ struct PhaseEnv {
     const float4 *rys; // smem [2][12] ry_entry(): round 0, round 1
     const float2 *mgs; // smem [2][3] group scales (M, M): round 0, round 1
     uint32_t rot;
+    bool scale;        // apply the group scales (false: folded into the diagonal)
     DiagCtx d;
     const float2 *treg_s;
+    const float *kc;   // smem [2][3] K scale corrections (nullptr = 1)
     double *acc_w;     // this warp's [2 rounds][12][8] accumulators
 };
+__device__ __forceinline__ float kcorr(const PhaseEnv &e, int r, int g) {
+    return e.kc ? e.kc[3 * r + g] : 1.f;
+}
 // OPS: 1 = round 0, 2 = diagonal, 4 = round 1 (compile-time, so the 16-register
 // arrays stay in place across the whole phase).
 template <int G, uint32_t OPS, bool FULL>
 __device__ __forceinline__ void phase_fwd(uint8_t *tile, uint32_t tau, const PhaseEnv &e) {
     float2 v[16];
     lds16<G>(tile, tau, v);
-    if (OPS & 1u) ry_round<G, false, FULL>(v, e.rys, e.rot, e.mgs[G]);
+    if (OPS & 1u) ry_round<G, false, FULL>(v, e.rys, e.rot, e.mgs[G], e.scale);
     if (OPS & 2u) apply_diag<false>(v, e.d, e.treg_s);
-    if (OPS & 4u) ry_round<G, false, FULL>(v, e.rys + 12, e.rot, e.mgs[3 + G]);
+    if (OPS & 4u) ry_round<G, false, FULL>(v, e.rys + 12, e.rot, e.mgs[3 + G], e.scale);
     sts16<G>(tile, tau, v);
 }
 template <int G, uint32_t OPS, bool FULL>
@@ -346,18 +350,18 @@ __device__ __forceinline__ void phase_bwd(uint8_t *pt, uint8_t *lt, uint32_t tau
     lds16<G>(pt, tau, p);
     lds16<G>(lt, tau, l);
     if (OPS & 4u) {
-        ry_round<G, true, FULL>(p, e.rys + 12, e.rot, e.mgs[3 + G]);
-        ry_round<G, true, FULL>(l, e.rys + 12, e.rot, e.mgs[3 + G]);
-        kmeasure<G, FULL>(p, l, e.rot, e.acc_w + 12 * 8);
+        ry_round<G, true, FULL>(p, e.rys + 12, e.rot, e.mgs[3 + G], e.scale);
+        ry_round<G, true, FULL>(l, e.rys + 12, e.rot, e.mgs[3 + G], e.scale);
+        kmeasure<G, FULL>(p, l, e.rot, e.acc_w + 12 * 8, kcorr(e, 1, G));
     }
     if (OPS & 2u) {
         apply_diag<true>(p, e.d, e.treg_s);
         apply_diag<true>(l, e.d, e.treg_s);
     }
     if (OPS & 1u) {
-        ry_round<G, true, FULL>(p, e.rys, e.rot, e.mgs[G]);
-        ry_round<G, true, FULL>(l, e.rys, e.rot, e.mgs[G]);
-        kmeasure<G, FULL>(p, l, e.rot, e.acc_w);
+        ry_round<G, true, FULL>(p, e.rys, e.rot, e.mgs[G], e.scale);
+        ry_round<G, true, FULL>(l, e.rys, e.rot, e.mgs[G], e.scale);
+        kmeasure<G, FULL>(p, l, e.rot, e.acc_w, kcorr(e, 0, G));
     }
     sts16<G>(pt, tau, p);
     sts16<G>(lt, tau, l);

@@ -20,6 +20,55 @@ using namespace dev;
 
 constexpr size_t kAccBytes = size_t(8) * 2 * 12 * 8 * sizeof(double); // [warp][round][bit][8]
 
+// Shared pass prologue: Ry tables (rys), group scales (mgs) and the diagonal's
+// register table (treg_s). When the pass applies a diagonal and the product F
+// of all its group scales is >= 2^-40, the scales are folded into the
+// diagonal (treg_s *= F) and the Ry rounds run unscaled: the tile is off by a
+// known factor f between the diagonal and the round ends (|f| <= 2^40, no
+// overflow), and the backward's K measurements, taken at f^2 x their true
+// value, get kc = 1/f^2. Returns the scale flag for PhaseEnv.
+__device__ bool pass_prologue(const PassParams &p, uint32_t tid, float4 *rys, float2 *treg_s,
+                              float2 *mgs, float *kc) {
+    if (tid < 24) {
+        const int r = tid / 12, lb = tid % 12;
+        const int s = r == 0 ? p.s0 : p.s1;
+        float4 v = make_float4(0.f, 0.f, 1.f, 0.f); // identity: t = 0, m = 1
+        if (s >= 0 && ((p.rot_mask >> lb) & 1u)) v = ry_entry(p.ry[size_t(s) * p.n + p.qmap[lb]]);
+        rys[tid] = v;
+    } else if (tid >= 40 && tid < 46) { // product of the factored m per (round, group)
+        const int r = (tid - 40) / 3, g = (tid - 40) % 3;
+        const int s = r == 0 ? p.s0 : p.s1;
+        float M = 1.f;
+        for (int b = 0; b < 4; ++b) {
+            const int lb = 4 * g + b;
+            if (s >= 0 && ((p.rot_mask >> lb) & 1u)) M *= ry_entry(p.ry[size_t(s) * p.n + p.qmap[lb]]).z;
+        }
+        mgs[tid - 40] = make_float2(M, M);
+    }
+    __syncthreads();
+    float F = 1.f;
+#pragma unroll
+    for (int i = 0; i < 6; ++i) F *= mgs[i].x;
+    const bool fold = p.dt != nullptr && F >= 0x1p-40f;
+    if (tid < 16) {
+        float2 t = p.dt ? p.dt->treg[tid] : make_float2(1.f, 0.f);
+        if (fold) t = make_float2(t.x * F, t.y * F);
+        treg_s[tid] = t;
+    } else if (tid == 16 && kc) { // backward order: phases nph-1 .. 0
+        float f = 1.f;
+        for (int i = 0; i < 6; ++i) kc[i] = 1.f;
+        if (fold)
+            for (int i = p.nph - 1; i >= 0; --i) {
+                const int g = p.ph[i].g, ops = p.ph[i].ops;
+                if (ops & 4) { f /= mgs[3 + g].x; kc[3 + g] = 1.f / (f * f); }
+                if (ops & 2) f *= F;
+                if (ops & 1) { f /= mgs[g].x; kc[g] = 1.f / (f * f); }
+            }
+    }
+    __syncthreads();
+    return !fold;
+}
+
 // Forward: 3 CTAs/SM, each double-buffered (load of tile i+1 overlaps tile i).
 // Backward, NB = 1: 2 CTAs/SM, single-buffered (psi + lambda = 64 KiB); the two
 // CTAs overlap each other's TMA traffic with compute. NB = 3: 1 CTA/SM with a
@@ -27,7 +76,7 @@ constexpr size_t kAccBytes = size_t(8) * 2 * 12 * 8 * sizeof(double); // [warp][
 // (QF_BWD_PIPE=3 for the ring).
 constexpr size_t pass_smem(bool bwd, int nb) {
     return size_t(nb) * kTileBytes * (bwd ? 2 : 1) + 64 /*mbar*/ + 24 * 16 /*rys*/ +
-           16 * 8 /*treg*/ + 8 * 8 /*mgs*/ + (bwd ? kAccBytes : 0) + 1024 /*align*/;
+           16 * 8 /*treg*/ + 8 * 8 /*mgs*/ + 32 /*kc*/ + (bwd ? kAccBytes : 0) + 1024 /*align*/;
 }
 constexpr int min_blocks(bool bwd, int nb) { return bwd ? (nb == 1 ? 2 : 1) : 3; }
 
@@ -44,40 +93,9 @@ __global__ void __launch_bounds__(kThreads, min_blocks(BWD, NB))
     float4 *rys = reinterpret_cast<float4 *>(tail + 64);
     float2 *treg_s = reinterpret_cast<float2 *>(tail + 64 + 24 * 16);
     float2 *mgs = treg_s + 16; // [2 rounds][3 groups]
-    double *acc = reinterpret_cast<double *>(tail + 64 + 24 * 16 + 16 * 8 + 8 * 8);
+    float *kc = reinterpret_cast<float *>(tail + 64 + 24 * 16 + 16 * 8 + 8 * 8);
+    double *acc = reinterpret_cast<double *>(tail + 64 + 24 * 16 + 16 * 8 + 8 * 8 + 32);
     const uint32_t tid = threadIdx.x, warp = tid >> 5;
-
-    if (tid < 24) {
-        const int r = tid / 12, lb = tid % 12;
-        const int s = r == 0 ? p.s0 : p.s1;
-        float4 v = make_float4(0.f, 0.f, 1.f, 0.f); // identity: t = 0, m = 1
-        if (s >= 0 && ((p.rot_mask >> lb) & 1u)) v = ry_entry(p.ry[size_t(s) * p.n + p.qmap[lb]]);
-        rys[tid] = v;
-    } else if (tid < 40) {
-        treg_s[tid - 24] = p.dt ? p.dt->treg[tid - 24] : make_float2(1.f, 0.f);
-    } else if (tid < 46) { // group scales: product of the factored m per (round, group)
-        const int r = (tid - 40) / 3, g = (tid - 40) % 3;
-        const int s = r == 0 ? p.s0 : p.s1;
-        float M = 1.f;
-        for (int b = 0; b < 4; ++b) {
-            const int lb = 4 * g + b;
-            if (s >= 0 && ((p.rot_mask >> lb) & 1u)) M *= ry_entry(p.ry[size_t(s) * p.n + p.qmap[lb]]).z;
-        }
-        mgs[tid - 40] = make_float2(M, M);
-    }
-    if (BWD) {
-        for (uint32_t i = tid; i < kAccBytes / 8; i += kThreads) acc[i] = 0.0;
-    }
-    const float2 tthr = p.dt ? p.dt->tthr[tid] : make_float2(1.f, 0.f);
-    const uint32_t thrinfo = p.cz ? p.cz->thrinfo[tid] : 0u;
-    if (tid == 0) {
-        prefetch_map(&m_in);
-        prefetch_map(&m_out);
-        if (BWD) prefetch_map(&m_lam);
-        for (int b = 0; b < NB; ++b) mbar_init(&mbar[b], 1);
-        fence_mbar_init();
-    }
-    __syncthreads();
 
     const int lo_mask = (1 << p.tile_lo_bits) - 1, hi_mask = (1 << p.tile_hi_bits) - 1;
     const int sample_shift = p.tile_lo_bits + p.tile_hi_bits;
@@ -90,15 +108,28 @@ __global__ void __launch_bounds__(kThreads, min_blocks(BWD, NB))
         if (BWD) tma_load5(dst + kTileBytes, &m_lam, &mbar[b], 0, c1, 0, c3, c4);
     };
     const int stride = gridDim.x;
-    if (tid == 0) {
+    if (tid == 0) { // first loads in flight before the prologue
+        prefetch_map(&m_in);
+        prefetch_map(&m_out);
+        if (BWD) prefetch_map(&m_lam);
+        for (int b = 0; b < NB; ++b) mbar_init(&mbar[b], 1);
+        fence_mbar_init();
         for (int b = 0; b < NB; ++b)
             if (int(blockIdx.x) + b * stride < p.tiles) issue_load(blockIdx.x + b * stride, b);
     }
+    if (BWD) {
+        for (uint32_t i = tid; i < kAccBytes / 8; i += kThreads) acc[i] = 0.0;
+    }
+    const bool scale = pass_prologue(p, tid, rys, treg_s, mgs, BWD ? kc : nullptr);
+    const float2 tthr = p.dt ? p.dt->tthr[tid] : make_float2(1.f, 0.f);
+    const uint32_t thrinfo = p.cz ? p.cz->thrinfo[tid] : 0u;
     PhaseEnv env;
     env.rys = rys;
     env.mgs = mgs;
     env.rot = p.rot_mask;
+    env.scale = scale;
     env.treg_s = treg_s;
+    env.kc = BWD ? kc : nullptr;
     env.acc_w = acc + warp * 2 * 12 * 8;
     env.d.base = make_float2(1.f, 0.f);
     env.d.sgn = 0;
@@ -159,7 +190,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks(BWD, NB))
 constexpr int kDualThreads = 2 * kThreads;
 constexpr size_t kDualAcc = size_t(16) * 2 * 12 * 8 * sizeof(double);
 constexpr size_t dual_smem() {
-    return size_t(3) * 2 * kTileBytes + 64 /*6 mbar*/ + 24 * 16 + 16 * 8 + 8 * 8 + kDualAcc + 1024;
+    return size_t(3) * 2 * kTileBytes + 64 /*6 mbar*/ + 24 * 16 + 16 * 8 + 8 * 8 + 32 + kDualAcc + 1024;
 }
 __device__ __forceinline__ void named_bar(int id, int n) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
@@ -177,40 +208,11 @@ __global__ void __launch_bounds__(kDualThreads, 1)
     float4 *rys = reinterpret_cast<float4 *>(tail + 64);
     float2 *treg_s = reinterpret_cast<float2 *>(tail + 64 + 24 * 16);
     float2 *mgs = treg_s + 16;
-    double *acc = reinterpret_cast<double *>(tail + 64 + 24 * 16 + 16 * 8 + 8 * 8);
+    float *kc = reinterpret_cast<float *>(tail + 64 + 24 * 16 + 16 * 8 + 8 * 8);
+    double *acc = reinterpret_cast<double *>(tail + 64 + 24 * 16 + 16 * 8 + 8 * 8 + 32);
     const uint32_t tid = threadIdx.x, warp = tid >> 5;
     const int half = int(tid >> 8);
     const uint32_t gtid = tid & 255u;
-
-    if (tid < 24) {
-        const int r = tid / 12, lb = tid % 12;
-        const int s = r == 0 ? p.s0 : p.s1;
-        float4 v = make_float4(0.f, 0.f, 1.f, 0.f);
-        if (s >= 0 && ((p.rot_mask >> lb) & 1u)) v = ry_entry(p.ry[size_t(s) * p.n + p.qmap[lb]]);
-        rys[tid] = v;
-    } else if (tid < 40) {
-        treg_s[tid - 24] = p.dt ? p.dt->treg[tid - 24] : make_float2(1.f, 0.f);
-    } else if (tid < 46) {
-        const int r = (tid - 40) / 3, g = (tid - 40) % 3;
-        const int s = r == 0 ? p.s0 : p.s1;
-        float M = 1.f;
-        for (int b = 0; b < 4; ++b) {
-            const int lb = 4 * g + b;
-            if (s >= 0 && ((p.rot_mask >> lb) & 1u)) M *= ry_entry(p.ry[size_t(s) * p.n + p.qmap[lb]]).z;
-        }
-        mgs[tid - 40] = make_float2(M, M);
-    }
-    for (uint32_t i = tid; i < kDualAcc / 8; i += kDualThreads) acc[i] = 0.0;
-    const float2 tthr = p.dt ? p.dt->tthr[gtid] : make_float2(1.f, 0.f);
-    const uint32_t thrinfo = p.cz ? p.cz->thrinfo[gtid] : 0u;
-    if (tid == 0) {
-        prefetch_map(&m_in);
-        prefetch_map(&m_out);
-        prefetch_map(&m_lam);
-        for (int b = 0; b < 6; ++b) mbar_init(&mbar[b], 1);
-        fence_mbar_init();
-    }
-    __syncthreads();
 
     const int lo_mask = (1 << p.tile_lo_bits) - 1, hi_mask = (1 << p.tile_hi_bits) - 1;
     const int sample_shift = p.tile_lo_bits + p.tile_hi_bits;
@@ -226,19 +228,35 @@ __global__ void __launch_bounds__(kDualThreads, 1)
         tma_load5(dst, &m_in, bar, 0, c1, 0, c3, c4);
         tma_load5(dst + kTileBytes, &m_lam, bar, 0, c1, 0, c3, c4);
     };
-    if (tid == 0)
+    if (tid == 0) { // first loads in flight before the prologue
+        prefetch_map(&m_in);
+        prefetch_map(&m_out);
+        prefetch_map(&m_lam);
+        for (int b = 0; b < 6; ++b) mbar_init(&mbar[b], 1);
+        fence_mbar_init();
         for (int k = 0; k < 3; ++k)
             if (tile_of(k) < p.tiles) issue_load(k);
+    }
+    for (uint32_t i = tid; i < kDualAcc / 8; i += kDualThreads) acc[i] = 0.0;
+    const bool scale = pass_prologue(p, tid, rys, treg_s, mgs, kc);
+    const float2 tthr = p.dt ? p.dt->tthr[gtid] : make_float2(1.f, 0.f);
+    const uint32_t thrinfo = p.cz ? p.cz->thrinfo[gtid] : 0u;
 
     PhaseEnv env;
     env.rys = rys;
     env.mgs = mgs;
     env.rot = p.rot_mask;
+    env.scale = scale;
     env.treg_s = treg_s;
+    env.kc = kc;
     env.acc_w = acc + warp * 2 * 12 * 8;
     env.d.base = make_float2(1.f, 0.f);
     env.d.sgn = 0;
     const int bar_id = 1 + half;
+    // The refill of a stored buffer (tile k + 3, for the other half) waits for
+    // the store's shared-memory read; it is deferred to the end of this half's
+    // next first phase, so no thread idles on the store.
+    int pending = -1;
     for (int k = half; tile_of(k) < p.tiles; k += 2) {
         const int t = tile_of(k);
         if (p.dt) env.d = diag_ctx(gtid, tthr, thrinfo, p.dt, p.cz, p.tileinfo, uint32_t(t) & tis_mask);
@@ -247,6 +265,11 @@ __global__ void __launch_bounds__(kDualThreads, 1)
         for (int i = p.nph - 1; i >= 0; --i) {
             if (i != p.nph - 1) named_bar(bar_id, kThreads);
             run_phase_bwd(p.ph[i].g, pt, pt + kTileBytes, gtid, p.ph[i].ops, env);
+            if (i == p.nph - 1 && gtid == 0 && pending >= 0) {
+                bulk_wait_read0();
+                issue_load(pending);
+                pending = -1;
+            }
         }
         fence_async_smem();
         named_bar(bar_id, kThreads);
@@ -255,13 +278,16 @@ __global__ void __launch_bounds__(kDualThreads, 1)
             if (p.write_psi) tma_store5(&m_out, pt, 0, c1, 0, c3, c4);
             tma_store5(&m_lam, pt + kTileBytes, 0, c1, 0, c3, c4);
             bulk_commit();
-            if (tile_of(k + 3) < p.tiles) {
-                bulk_wait_read0();
-                issue_load(k + 3);
-            }
+            if (tile_of(k + 3) < p.tiles) pending = k + 3;
         }
     }
-    if (gtid == 0) bulk_wait0();
+    if (gtid == 0) {
+        if (pending >= 0) { // unreachable: k + 3 exists only if k + 2 does
+            bulk_wait_read0();
+            issue_load(pending);
+        }
+        bulk_wait0();
+    }
     __syncthreads();
     if (tid < 2 * 12 * 8) {
         const int r = tid / 96, lb = (tid / 8) % 12, c = tid & 7;
