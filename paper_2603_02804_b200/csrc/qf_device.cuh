@@ -223,7 +223,7 @@ __device__ __forceinline__ float4 ry_entry(float2 cs) {
 // 6 FFMA2 per pair into ONE accumulator per output (measured 29 vs 24 TFMA/s
 // for two interleaved sets, tools/ffma2_patterns.cu); the four bits of a
 // group give 12 independent chains.
-template <int B>
+template <int B, bool WZ>
 __device__ __forceinline__ void kbit3(const float2 (&p)[16], const float2 (&l)[16], float *out) {
     float2 bx = make_float2(0.f, 0.f), ay = bx, bz = bx;
 #pragma unroll
@@ -231,38 +231,86 @@ __device__ __forceinline__ void kbit3(const float2 (&p)[16], const float2 (&l)[1
         if (j & (1 << B)) continue;
         const int j1 = j | (1 << B);
         const float2 ps0 = make_float2(p[j].y, p[j].x), ps1 = make_float2(p[j1].y, p[j1].x);
-        bz = f2fma(ps0, l[j], bz);
+        if (WZ) bz = f2fma(ps0, l[j], bz);
         bx = f2fma(ps0, l[j1], bx);
         ay = f2fma(p[j], l[j1], ay);
         ay = f2fma(make_float2(-p[j1].x, -p[j1].y), l[j], ay);
         bx = f2fma(ps1, l[j], bx);
-        bz = f2fma(make_float2(-ps1.x, -ps1.y), l[j1], bz);
+        if (WZ) bz = f2fma(make_float2(-ps1.x, -ps1.y), l[j1], bz);
     }
     out[0] = bx.x - bx.y;
     out[1] = ay.x + ay.y;
-    out[2] = bz.x - bz.y;
+    if (WZ) out[2] = bz.x - bz.y;
+}
+
+// All four register bits at once, lambda-major: the 12 FFMA2 that read l[j]
+// run back to back, so l[j] stays in the operand reuse cache and each FFMA2
+// fetches two fresh register pairs (three would cost a third issue cycle;
+// measured 30.8 vs 29.0 TFMA/s, tools/ffma2_patterns.cu). 12 accumulators,
+// each updated every 12th instruction.
+template <bool WZ>
+__device__ __forceinline__ void kbit3_all(const float2 (&p)[16], const float2 (&l)[16], float *out) {
+    constexpr int C = WZ ? 3 : 2; // outputs per bit: X, Y (, Z)
+    float2 r[12];
+#pragma unroll
+    for (int i = 0; i < 12; ++i) r[i] = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const int k = j ^ (1 << b);
+            const float2 psj = make_float2(p[j].y, p[j].x), psk = make_float2(p[k].y, p[k].x);
+            float2 &bx = r[C * b], &ay = r[C * b + 1], &bz = r[C * b + C - 1];
+            if (!(j & (1 << b))) { // l[j] = lambda_0 of the pair
+                if (WZ) bz = f2fma(psj, l[j], bz);
+                bx = f2fma(psk, l[j], bx);
+                ay = f2fma(make_float2(-p[k].x, -p[k].y), l[j], ay);
+            } else {               // l[j] = lambda_1 of the pair
+                if (WZ) bz = f2fma(make_float2(-psj.x, -psj.y), l[j], bz);
+                bx = f2fma(psk, l[j], bx);
+                ay = f2fma(p[k], l[j], ay);
+            }
+        }
+    }
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+        out[C * b + 0] = r[C * b].x - r[C * b].y;
+        out[C * b + 1] = r[C * b + 1].x + r[C * b + 1].y;
+        if (WZ) out[C * b + 2] = r[C * b + 2].x - r[C * b + 2].y;
+    }
 }
 
 // (X, Y, Z) of the rotated bits of group G at the current point: 12 values
 // reduced over the warp in one 16-wide reduce-scatter (16 shuffles), then
 // added in fp64 (times kc, the pass's scale correction) to this warp's
 // accumulator acc_w[local bit][8] (slots 0..2).
-template <int G, bool FULL>
+//
+// WZ = false measures only (X, Y) (8 values, 9 shuffles): Z commutes with the
+// diagonals and with every gate on other qubits, so Z before Ry_s(q) equals Z
+// just after Ry_{s-1}(q) = cos(b) Z_{s-1} - sin(b) X_{s-1} (b = beta_{s-1}(q)),
+// rebuilt per qubit by zchain_kernel; only stage 0 measures Z.
+template <int G, bool FULL, bool WZ>
 __device__ __forceinline__ void kmeasure(const float2 (&p)[16], const float2 (&l)[16],
                                          uint32_t rot, double *acc_w, float kc) {
 #if QF_ABLATE_K
     return; // timing ablation only
 #endif
-    float v[16];
+    constexpr int C = WZ ? 3 : 2;
+    constexpr int NV = WZ ? 16 : 8; // reduce width
+    float v[NV];
 #pragma unroll
-    for (int i = 0; i < 16; ++i) v[i] = 0.f;
-    if (FULL || (rot & (1u << (4 * G + 0)))) kbit3<0>(p, l, v + 0);
-    if (FULL || (rot & (1u << (4 * G + 1)))) kbit3<1>(p, l, v + 3);
-    if (FULL || (rot & (1u << (4 * G + 2)))) kbit3<2>(p, l, v + 6);
-    if (FULL || (rot & (1u << (4 * G + 3)))) kbit3<3>(p, l, v + 9);
+    for (int i = 0; i < NV; ++i) v[i] = 0.f;
+    if (FULL) {
+        kbit3_all<WZ>(p, l, v);
+    } else {
+        if (rot & (1u << (4 * G + 0))) kbit3<0, WZ>(p, l, v + 0 * C);
+        if (rot & (1u << (4 * G + 1))) kbit3<1, WZ>(p, l, v + 1 * C);
+        if (rot & (1u << (4 * G + 2))) kbit3<2, WZ>(p, l, v + 2 * C);
+        if (rot & (1u << (4 * G + 3))) kbit3<3, WZ>(p, l, v + 3 * C);
+    }
     const uint32_t lane = threadIdx.x & 31u;
 #pragma unroll
-    for (int m = 8; m >= 1; m >>= 1) {
+    for (int m = NV / 2; m >= 1; m >>= 1) {
         const bool up = (lane & m) != 0;
 #pragma unroll
         for (int i = 0; i < m; ++i) {
@@ -271,9 +319,11 @@ __device__ __forceinline__ void kmeasure(const float2 (&p)[16], const float2 (&l
             v[i] = keep + __shfl_xor_sync(0xffffffffu, send, m);
         }
     }
-    const float r = v[0] + __shfl_xor_sync(0xffffffffu, v[0], 16);
-    if (lane < 12) {
-        const uint32_t bit = lane / 3u, comp = lane % 3u;
+    float r = v[0];
+#pragma unroll
+    for (int m = NV; m < 32; m <<= 1) r += __shfl_xor_sync(0xffffffffu, r, m);
+    if (lane < uint32_t(4 * C)) {
+        const uint32_t bit = lane / uint32_t(C), comp = lane % uint32_t(C);
         if (rot & (1u << (4 * G + bit))) acc_w[(4 * G + bit) * 8 + comp] += double(r) * double(kc);
     }
 }
@@ -328,6 +378,7 @@ struct PhaseEnv {
     DiagCtx d;
     const float2 *treg_s;
     const float *kc;   // smem [2][3] K scale corrections (nullptr = 1)
+    uint32_t zm;       // bit r: round r measures Z (stage 0 only; zchain_kernel)
     double *acc_w;     // this warp's [2 rounds][12][8] accumulators
 };
 __device__ __forceinline__ float kcorr(const PhaseEnv &e, int r, int g) {
@@ -352,7 +403,8 @@ __device__ __forceinline__ void phase_bwd(uint8_t *pt, uint8_t *lt, uint32_t tau
     if (OPS & 4u) {
         ry_round<G, true, FULL>(p, e.rys + 12, e.rot, e.mgs[3 + G], e.scale);
         ry_round<G, true, FULL>(l, e.rys + 12, e.rot, e.mgs[3 + G], e.scale);
-        kmeasure<G, FULL>(p, l, e.rot, e.acc_w + 12 * 8, kcorr(e, 1, G));
+        if (e.zm & 2u) kmeasure<G, FULL, true>(p, l, e.rot, e.acc_w + 12 * 8, kcorr(e, 1, G));
+        else kmeasure<G, FULL, false>(p, l, e.rot, e.acc_w + 12 * 8, kcorr(e, 1, G));
     }
     if (OPS & 2u) {
         apply_diag<true>(p, e.d, e.treg_s);
@@ -361,7 +413,8 @@ __device__ __forceinline__ void phase_bwd(uint8_t *pt, uint8_t *lt, uint32_t tau
     if (OPS & 1u) {
         ry_round<G, true, FULL>(p, e.rys, e.rot, e.mgs[G], e.scale);
         ry_round<G, true, FULL>(l, e.rys, e.rot, e.mgs[G], e.scale);
-        kmeasure<G, FULL>(p, l, e.rot, e.acc_w, kcorr(e, 0, G));
+        if (e.zm & 1u) kmeasure<G, FULL, true>(p, l, e.rot, e.acc_w, kcorr(e, 0, G));
+        else kmeasure<G, FULL, false>(p, l, e.rot, e.acc_w, kcorr(e, 0, G));
     }
     sts16<G>(pt, tau, p);
     sts16<G>(lt, tau, l);

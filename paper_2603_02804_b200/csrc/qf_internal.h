@@ -78,6 +78,7 @@ struct PassParams {
     const CzTab *cz;   // its CZ set in this layout (nullptr = none)
     const uint32_t *tileinfo;
     int write_psi;     // backward: store psi (0 when the next reader is a slot)
+    int zmask;         // backward: bit r = round r measures Z (its stage is 0)
     double *kpart;     // backward: [grid][stages][n][8]
     long long kstride; // stages*n*8
 };
@@ -142,6 +143,9 @@ cudaError_t launch_finalize(cudaStream_t st, int n_sec, const uint32_t *sec_q,
                             const double *expect, uint32_t batch, double *loss);
 cudaError_t launch_random_state(cudaStream_t st, uint64_t seed, uint64_t first_sample, int n,
                                 uint32_t batch, double *scratch, float2 *out);
+// Z of every (stage >= 1, qubit) from the previous stage's (X, Z) and Ry angle
+// (qf_device.cuh kmeasure): streaming plans measure Z at stage 0 only.
+cudaError_t launch_zchain(cudaStream_t st, int stages, int n, const float2 *ry, double *kout);
 int pass_occupancy(bool backward);
 int resident_occupancy();
 size_t pass_smem_bytes(bool backward);

@@ -130,6 +130,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks(BWD, NB))
     env.scale = scale;
     env.treg_s = treg_s;
     env.kc = BWD ? kc : nullptr;
+    env.zm = uint32_t(p.zmask);
     env.acc_w = acc + warp * 2 * 12 * 8;
     env.d.base = make_float2(1.f, 0.f);
     env.d.sgn = 0;
@@ -249,6 +250,7 @@ __global__ void __launch_bounds__(kDualThreads, 1)
     env.scale = scale;
     env.treg_s = treg_s;
     env.kc = kc;
+    env.zm = uint32_t(p.zmask);
     env.acc_w = acc + warp * 2 * 12 * 8;
     env.d.base = make_float2(1.f, 0.f);
     env.d.sgn = 0;

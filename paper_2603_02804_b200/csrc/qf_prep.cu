@@ -179,6 +179,24 @@ __global__ void finalize_kernel(int n_sec, const uint32_t *sec_q, const uint32_t
     }
 }
 
+// Z(s) = cos(b) Z(s-1) - sin(b) X(s-1), b = beta_{s-1}(q): Z commutes with every
+// diagonal and every other qubit's gate between Ry_{s-1}(q) and Ry_s(q), and
+// Ry(b)^dag sz Ry(b) = cos(b) sz - sin(b) sx. One thread per qubit, in stage order.
+__global__ void zchain_kernel(int stages, int n, const float2 *__restrict__ ry,
+                              double *__restrict__ kout) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= n) return;
+    double z = kout[size_t(q) * 8 + 2]; // stage 0: measured
+#pragma unroll 8
+    for (int s = 1; s < stages; ++s) {
+        const float2 cs = __ldg(&ry[size_t(s - 1) * n + q]);
+        const double x = kout[(size_t(s - 1) * n + q) * 8];
+        const double c = cs.x, sn = cs.y;
+        z = (c * c - sn * sn) * z - (2.0 * c * sn) * x;
+        kout[(size_t(s) * n + q) * 8 + 2] = z;
+    }
+}
+
 __device__ __forceinline__ uint64_t sm_mix(uint64_t z) {
     z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
     z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
@@ -268,6 +286,12 @@ cudaError_t launch_finalize(cudaStream_t st, int n_sec, const uint32_t *sec_q,
         finalize_kernel<<<(n_sec + 127) / 128, 128, 0, st>>>(n_sec, sec_q, sec_stage, sec_off,
                                                              sec_gates, sec_gamma, theta, n, kout,
                                                              grad, loss);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_zchain(cudaStream_t st, int stages, int n, const float2 *ry, double *kout) {
+    if (stages <= 1 || n <= 0) return cudaSuccess;
+    zchain_kernel<<<1, 32, 0, st>>>(stages, n, ry, kout);
     return cudaGetLastError();
 }
 

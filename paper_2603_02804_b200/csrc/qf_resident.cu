@@ -166,6 +166,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         e.rot = rot;
         e.scale = true;
         e.kc = nullptr;
+        e.zm = 3u;
         e.treg_s = treg_s + sl * 16;
         e.acc_w = acc + warp * 2 * 12 * 8;
         const int c = p.stage_cz[s];

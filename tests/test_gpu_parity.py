@@ -287,3 +287,19 @@ def test_deep_circuit_uncompute_drift(ctx, oracle):
     gates, npar, theta, psi0, pauli = _hea_case(n, layers, 1, seed=77)
     res = capi.gradient_c64(ctx, gates, n, npar, layers, 10, psi0, theta, pauli)
     _check(res, oracle.gradient(gates, n, npar, psi0, theta, pauli))
+
+
+def test_config4_depth_fused_vs_pergate(ctx):
+    """BASELINE config 4 depth (20q x 1000 layers, k = 10) on a 2-sample shard:
+    the fused path (X, Y measured, Z chained over 1000 stages, scales folded
+    into the diagonals) against the independent per-gate comparator (one
+    kernel per gate, 80,000 gates each way). The CPU oracle would need ~10 min
+    here, so this is the size-independent cross-check at full depth."""
+    n, layers, batch = 20, 1000, 2
+    gates, npar, theta, psi0, pauli = _hea_case(n, layers, batch, seed=4242)
+    fused = capi.gradient_c64(ctx, gates, n, npar, layers, 10, psi0, theta, pauli)
+    pg = capi.gradient_c64(ctx, gates, n, npar, layers, 0, psi0, theta, pauli, pergate=True)
+    err = rel_diff(fused.gradient, pg.gradient)
+    assert err <= TOL, err
+    assert rel_diff(fused.expect, pg.expect) <= TOL
+    assert np.all(np.isfinite(fused.gradient))

@@ -40,10 +40,10 @@ __global__ void __launch_bounds__(512, 1) pat(float *out, int iters, float4 e) {
 #pragma unroll
             for (int j = 0; j < 16; ++j) ps[j] = make_float2(p[j].y, p[j].x);
             float v[12];
-            kbit3<0>(p, ps, l, v + 0);
-            kbit3<1>(p, ps, l, v + 3);
-            kbit3<2>(p, ps, l, v + 6);
-            kbit3<3>(p, ps, l, v + 9);
+            kbit3<0>(p, l, v + 0);
+            kbit3<1>(p, l, v + 3);
+            kbit3<2>(p, l, v + 6);
+            kbit3<3>(p, l, v + 9);
 #pragma unroll
             for (int i = 0; i < 12; ++i) acc[i] += v[i];
         }
@@ -209,6 +209,34 @@ __global__ void __launch_bounds__(512, 1) pat(float *out, int iters, float4 e) {
                 acc[3 * b + 2] += a[4 * b + 2] - a[4 * b + 3];
             }
         }
+        if (K == 10) { // lambda-major: l[j] reused in slot B by 12 consecutive FFMA2
+            float2 r[12];
+#pragma unroll
+            for (int i = 0; i < 12; ++i) r[i] = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {
+                    const int k = j ^ (1 << b);
+                    const float2 psj = make_float2(p[j].y, p[j].x), psk = make_float2(p[k].y, p[k].x);
+                    float2 &bx = r[3 * b], &ay = r[3 * b + 1], &bz = r[3 * b + 2];
+                    if (!(j & (1 << b))) {
+                        bz = __ffma2_rn(psj, l[j], bz);
+                        bx = __ffma2_rn(psk, l[j], bx);
+                        ay = __ffma2_rn(make_float2(-p[k].x, -p[k].y), l[j], ay);
+                    } else {
+                        bz = __ffma2_rn(make_float2(-psj.x, -psj.y), l[j], bz);
+                        bx = __ffma2_rn(psk, l[j], bx);
+                        ay = __ffma2_rn(p[k], l[j], ay);
+                    }
+                }
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                acc[3 * b] += r[3 * b].x - r[3 * b].y;
+                acc[3 * b + 1] += r[3 * b + 1].x + r[3 * b + 1].y;
+                acc[3 * b + 2] += r[3 * b + 2].x - r[3 * b + 2].y;
+            }
+        }
         if (K == 8 || K == 9) { // 8: no swaps/negations (timing only); 9: swaps, no negations (split acc)
             float2 r[16];
 #pragma unroll
@@ -279,6 +307,7 @@ int main() {
     run<7>(o, "Ry + K hybrid (Y FFMA2, X/Z FFMA)");
     run<8>(o, "Ry + K FFMA2 no swap/neg (timing only)");
     run<9>(o, "Ry + K FFMA2 swaps, no negation");
+    run<10>(o, "Ry + K lambda-major (l reused)");
     printf("err: %s\n", cudaGetErrorString(cudaGetLastError()));
     return 0;
 }

@@ -14,7 +14,69 @@
 using namespace qfb;
 using namespace qfb::dev;
 
-template <int MODE, bool SCALE = true> // MODE 0 = named barriers between phases, 1 = none (timing only)
+template <int G, uint32_t OPS, int M>
+__device__ __forceinline__ void phase_var(uint8_t *pt, uint8_t *lt, uint32_t tau, const PhaseEnv &e,
+                                          float2 (&p)[16], float2 (&l)[16]) {
+    if (M != 2) { lds16<G>(pt, tau, p); lds16<G>(lt, tau, l); }
+    if (M != 3) {
+        if (OPS & 4u) {
+            ry_round<G, true, true>(p, e.rys + 12, e.rot, e.mgs[3 + G], e.scale);
+            ry_round<G, true, true>(l, e.rys + 12, e.rot, e.mgs[3 + G], e.scale);
+            kmeasure<G, true>(p, l, e.rot, e.acc_w + 12 * 8, 1.f);
+        }
+        if (OPS & 2u) { apply_diag<true>(p, e.d, e.treg_s); apply_diag<true>(l, e.d, e.treg_s); }
+        if (OPS & 1u) {
+            ry_round<G, true, true>(p, e.rys, e.rot, e.mgs[G], e.scale);
+            ry_round<G, true, true>(l, e.rys, e.rot, e.mgs[G], e.scale);
+            kmeasure<G, true>(p, l, e.rot, e.acc_w, 1.f);
+        }
+    }
+    if (M != 2) { sts16<G>(pt, tau, p); sts16<G>(lt, tau, l); }
+}
+template <int M>
+__global__ void __launch_bounds__(512, 1) probe_var(const DiagTab *dt, int iters, float *out) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = align1024(smem_raw);
+    float4 *rys = reinterpret_cast<float4 *>(smem + 4 * kTileBytes);
+    float2 *treg_s = reinterpret_cast<float2 *>(rys + 24);
+    float2 *mgs = treg_s + 16;
+    double *acc = reinterpret_cast<double *>(mgs + 8);
+    const uint32_t tid = threadIdx.x, half = tid >> 8, gtid = tid & 255u, warp = tid >> 5;
+    if (tid < 24) rys[tid] = ry_entry(make_float2(0.9f + 0.001f * tid, 0.3f));
+    if (tid < 16) treg_s[tid] = dt->treg[tid];
+    if (tid < 6) mgs[tid] = make_float2(0.7f, 0.7f);
+    for (uint32_t i = tid; i < 16 * 2 * 12 * 8; i += 512) acc[i] = 0.0;
+    uint8_t *pt = smem + half * 2 * kTileBytes;
+    for (uint32_t i = gtid; i < 2 * kTileAmps; i += 256)
+        reinterpret_cast<float2 *>(pt)[i] = make_float2(1e-3f * (i & 7), 1e-3f);
+    __syncthreads();
+    PhaseEnv env;
+    env.rys = rys; env.mgs = mgs; env.rot = 0xFFFu; env.scale = false; env.kc = nullptr;
+    env.treg_s = treg_s; env.acc_w = acc + warp * 2 * 12 * 8;
+    env.d = diag_ctx(gtid, dt->tthr[gtid], 0u, dt, nullptr, nullptr, blockIdx.x & 255u);
+    float2 p[16], l[16];
+    for (int j = 0; j < 16; ++j) { p[j] = make_float2(1e-3f * j, gtid * 1e-6f); l[j] = p[j]; }
+    uint8_t *lt = pt + kTileBytes;
+    for (int it = 0; it < iters; ++it) {
+        phase_var<2, 4, M>(pt, lt, gtid, env, p, l);
+        asm volatile("bar.sync %0, 256;" ::"r"(1 + int(half)) : "memory");
+        phase_var<1, 4, M>(pt, lt, gtid, env, p, l);
+        asm volatile("bar.sync %0, 256;" ::"r"(1 + int(half)) : "memory");
+        phase_var<0, 7, M>(pt, lt, gtid, env, p, l);
+        asm volatile("bar.sync %0, 256;" ::"r"(1 + int(half)) : "memory");
+        phase_var<2, 1, M>(pt, lt, gtid, env, p, l);
+        asm volatile("bar.sync %0, 256;" ::"r"(1 + int(half)) : "memory");
+        phase_var<1, 1, M>(pt, lt, gtid, env, p, l);
+        asm volatile("bar.sync %0, 256;" ::"r"(1 + int(half)) : "memory");
+    }
+    __syncthreads();
+    float s = 0;
+    for (int j = 0; j < 16; ++j) s += p[j].x + l[j].y;
+    if (tid == 0) out[blockIdx.x] = float(acc[0]) + reinterpret_cast<float *>(pt)[5] + s;
+    else if (s == 123.f) out[1] = s;
+}
+
+template <int MODE, bool SCALE = true, int SKEW = 0> // MODE 0 = named barriers between phases, 1 = none (timing only)
 __global__ void __launch_bounds__(512, 1) probe(const DiagTab *dt, int iters, float *out) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = align1024(smem_raw);
@@ -40,6 +102,10 @@ __global__ void __launch_bounds__(512, 1) probe(const DiagTab *dt, int iters, fl
     env.treg_s = treg_s;
     env.acc_w = acc + warp * 2 * 12 * 8;
     env.d = diag_ctx(gtid, dt->tthr[gtid], 0u, dt, nullptr, nullptr, blockIdx.x & 255u);
+    if (SKEW && half) { // start half 1 SKEW cycles late
+        const long long t0 = clock64();
+        while (clock64() - t0 < SKEW) {}
+    }
     const int G[5] = {1, 2, 0, 1, 2};
     const int O[5] = {1, 1, 7, 4, 4};
     for (int it = 0; it < iters; ++it) {
@@ -105,6 +171,20 @@ int main() {
     cudaEventCreate(&e1);
     const int iters = 200;
     cudaFuncSetAttribute(probe<0, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    cudaFuncSetAttribute(probe<0, false, 2000>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    cudaFuncSetAttribute(probe<0, false, 5000>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    cudaFuncSetAttribute(probe<0, false, 12000>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    for (int sk = 0; sk < 3; ++sk) {
+        cudaEventRecord(e0);
+        if (sk == 0) probe<0, false, 2000><<<148, 512, smem>>>(d, iters, o);
+        if (sk == 1) probe<0, false, 5000><<<148, 512, smem>>>(d, iters, o);
+        if (sk == 2) probe<0, false, 12000><<<148, 512, smem>>>(d, iters, o);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        printf("skew %d: %.3f ms  %.1f us/tile/half\n", sk == 0 ? 2000 : sk == 1 ? 5000 : 12000, ms, ms * 1e3 / iters);
+    }
     for (int rep = 0; rep < 2; ++rep) {
         cudaEventRecord(e0);
         probe<0, false><<<148, 512, smem>>>(d, iters, o);
@@ -113,6 +193,22 @@ int main() {
         float ms;
         cudaEventElapsedTime(&ms, e0, e1);
         printf("mode bar, scales folded: %.3f ms  %.1f us/tile/half\n", ms, ms * 1e3 / iters);
+    }
+    for (int m = 1; m <= 3; ++m) {
+        if (m == 1) cudaFuncSetAttribute(probe_var<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        if (m == 2) cudaFuncSetAttribute(probe_var<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        if (m == 3) cudaFuncSetAttribute(probe_var<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        for (int rep = 0; rep < 2; ++rep) {
+            cudaEventRecord(e0);
+            if (m == 1) probe_var<1><<<148, 512, smem>>>(d, iters, o);
+            if (m == 2) probe_var<2><<<148, 512, smem>>>(d, iters, o);
+            if (m == 3) probe_var<3><<<148, 512, smem>>>(d, iters, o);
+            cudaEventRecord(e1);
+            cudaEventSynchronize(e1);
+            float ms;
+            cudaEventElapsedTime(&ms, e0, e1);
+            printf("variant %s: %.1f us/tile/half\n", m == 1 ? "full" : m == 2 ? "compute only" : "smem only", ms * 1e3 / iters);
+        }
     }
     for (int mode = 0; mode < 2; ++mode)
         for (int rep = 0; rep < 3; ++rep) {
