@@ -22,13 +22,13 @@ __device__ __forceinline__ void phase_var(uint8_t *pt, uint8_t *lt, uint32_t tau
         if (OPS & 4u) {
             ry_round<G, true, true>(p, e.rys + 12, e.rot, e.mgs[3 + G], e.scale);
             ry_round<G, true, true>(l, e.rys + 12, e.rot, e.mgs[3 + G], e.scale);
-            kmeasure<G, true>(p, l, e.rot, e.acc_w + 12 * 8, 1.f);
+            kmeasure<G, true, false>(p, l, e.rot, e.acc_w + 12 * 8, 1.f);
         }
         if (OPS & 2u) { apply_diag<true>(p, e.d, e.treg_s); apply_diag<true>(l, e.d, e.treg_s); }
         if (OPS & 1u) {
             ry_round<G, true, true>(p, e.rys, e.rot, e.mgs[G], e.scale);
             ry_round<G, true, true>(l, e.rys, e.rot, e.mgs[G], e.scale);
-            kmeasure<G, true>(p, l, e.rot, e.acc_w, 1.f);
+            kmeasure<G, true, false>(p, l, e.rot, e.acc_w, 1.f);
         }
     }
     if (M != 2) { sts16<G>(pt, tau, p); sts16<G>(lt, tau, l); }
@@ -51,7 +51,7 @@ __global__ void __launch_bounds__(512, 1) probe_var(const DiagTab *dt, int iters
         reinterpret_cast<float2 *>(pt)[i] = make_float2(1e-3f * (i & 7), 1e-3f);
     __syncthreads();
     PhaseEnv env;
-    env.rys = rys; env.mgs = mgs; env.rot = 0xFFFu; env.scale = false; env.kc = nullptr;
+    env.rys = rys; env.mgs = mgs; env.rot = 0xFFFu; env.scale = false; env.kc = nullptr; env.zm = 0;
     env.treg_s = treg_s; env.acc_w = acc + warp * 2 * 12 * 8;
     env.d = diag_ctx(gtid, dt->tthr[gtid], 0u, dt, nullptr, nullptr, blockIdx.x & 255u);
     float2 p[16], l[16];
@@ -99,6 +99,7 @@ __global__ void __launch_bounds__(512, 1) probe(const DiagTab *dt, int iters, fl
     env.rot = 0xFFFu;
     env.scale = SCALE;
     env.kc = nullptr;
+    env.zm = 0;
     env.treg_s = treg_s;
     env.acc_w = acc + warp * 2 * 12 * 8;
     env.d = diag_ctx(gtid, dt->tthr[gtid], 0u, dt, nullptr, nullptr, blockIdx.x & 255u);
