@@ -178,6 +178,7 @@ def workload_config(args, wl):
             "qubits": wl["n"], "layers": wl["layers"], "params": 3 * wl["n"] * wl["layers"],
             "batch_per_gpu": wl["batch"], "global_batch": wl["batch"] * args.gpus,
             "ckpt_layers": wl["ckpt"], "observable": "IXYZ repeated",
+            "storage": getattr(args, "storage", "full"),
             "l2": "inputs larger than L2 (state per GPU > 126 MB)" if wl["n"] >= 16
             else "state fits L2/smem (sample-resident)",
             "parallelism": f"dp{args.gpus}"}
@@ -217,7 +218,7 @@ def run_ours(args):
     gates, M = C.build_hea(n, layers)
     pauli = C.parse_pauli(C.repeated_ixyz_label(n))
     ctx = pkg.Context(dev)
-    plan = pkg.Plan(ctx, gates, n, M, layers, wl["ckpt"], B, pauli)
+    plan = pkg.Plan(ctx, gates, n, M, layers, wl["ckpt"], B, pauli, storage=args.storage)
     plan.random_psi0(SEED_STATE, first_sample=rank * B)
     theta_h = torch.from_numpy(C.random_parameters(M, SEED_THETA)).pin_memory()
     theta_d = theta_h.to("cuda")
@@ -377,6 +378,8 @@ def main():
     ap.add_argument("--layers", type=int, default=0, help="override layer count")
     ap.add_argument("--ckpt", type=int, default=None, help="override checkpoint layers")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--storage", default="full", choices=["full", "memsave"],
+                    help="StorageMode: memsave keeps checkpoint slots in bf16")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

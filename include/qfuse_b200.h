@@ -47,6 +47,14 @@ extern "C" {
 #define QF_EDEVICE 4
 
 enum { QF_GATE_ROTATION = 0, QF_GATE_CZ = 1, QF_GATE_CNOT = 2 };
+/* qfuse::StorageMode (engine.hpp:30). MEMSAVE keeps the checkpoint slots as
+ * bfloat16 (narrow_to_bf16, statevec.hpp:36-45; half the slot memory); compute
+ * and the final state stay complex64. The reference narrows its per-op ledger
+ * instead (engine.cpp:488-513); both are held to the same tolerance (5e-3 of
+ * the fp32 gradient, acceptance.cpp:466-499). Sample-resident plans (n <= 12)
+ * store nothing per layer off-chip and run MEMSAVE at full precision. */
+#define QF_STORAGE_FULL 0
+#define QF_STORAGE_MEMSAVE 1
 enum { QF_AXIS_X = 0, QF_AXIS_Y = 1, QF_AXIS_Z = 2 };
 
 /* One flattened gate (qfuse::Gate, circuit.hpp:28-49). 16 bytes. */
@@ -97,6 +105,12 @@ int qf_gradient_c64(qf_ctx *ctx, const qf_gate *gates, size_t n_gates, uint32_t 
                     uint64_t x_mask, uint64_t z_mask, double *loss_out, double *grad_out,
                     double *expect_out, qf_stats *stats_out);
 
+/* Same with the reference's StorageMode (QF_STORAGE_*). */
+int qf_gradient_c64_ex(qf_ctx *ctx, const qf_gate *gates, size_t n_gates, uint32_t n_qubits,
+                       uint32_t n_params, uint32_t layers, uint32_t ckpt_layers,
+                       uint32_t storage_mode, const float *psi0, uint32_t batch,
+                       const double *theta, uint64_t x_mask, uint64_t z_mask, double *loss_out,
+                       double *grad_out, double *expect_out, qf_stats *stats_out);
 /* Per-gate (unfused) comparator: one HBM traversal per gate, the
  * reference's naive_gradient (engine.cpp:856-894). Same arguments. */
 int qf_gradient_pergate_c64(qf_ctx *ctx, const qf_gate *gates, size_t n_gates,
@@ -113,6 +127,10 @@ int qf_gradient_pergate_c64(qf_ctx *ctx, const qf_gate *gates, size_t n_gates,
 int qf_plan_create(qf_ctx *ctx, const qf_gate *gates, size_t n_gates, uint32_t n_qubits,
                    uint32_t n_params, uint32_t layers, uint32_t ckpt_layers, uint32_t batch,
                    uint64_t x_mask, uint64_t z_mask, qf_plan **out);
+/* Same with the reference's StorageMode (QF_STORAGE_*). */
+int qf_plan_create_ex(qf_ctx *ctx, const qf_gate *gates, size_t n_gates, uint32_t n_qubits,
+                      uint32_t n_params, uint32_t layers, uint32_t ckpt_layers, uint32_t batch,
+                      uint64_t x_mask, uint64_t z_mask, uint32_t storage_mode, qf_plan **out);
 int qf_plan_destroy(qf_plan *plan);
 /* Batch store input. Host (pageable or pinned) -> device copy. */
 int qf_plan_upload_psi0(qf_plan *plan, const float *psi0_host);
@@ -147,7 +165,8 @@ int qf_plan_download_psi0(qf_plan *plan, float *psi0_host);
 
 /* Per-launch CUDA-event profiling by kernel kind (for roofline reporting).
  * Kinds: 0 forward pass, 1 backward pass, 2 observable, 3 sample-resident,
- * 4 prep/reduce/finalize, 5 per-gate. bytes = algorithmic HBM bytes. */
+ * 4 prep/reduce/finalize, 5 per-gate, 6 MemSave slot narrow/widen.
+ * bytes = algorithmic HBM bytes. */
 typedef struct qf_profile {
     uint64_t launches[8];
     double ms[8];

@@ -22,7 +22,8 @@ QF_OK, QF_EINVAL, QF_ECAPACITY, QF_EDEVICE = 0, 2, 3, 4
 # exported symbols, in include/qfuse_b200.h order
 SYMBOLS = (
     "qf_last_error", "qf_version", "qf_ctx_create", "qf_ctx_destroy", "qf_ctx_set_hbm_limit",
-    "qf_gradient_c64", "qf_gradient_pergate_c64", "qf_plan_create", "qf_plan_destroy",
+    "qf_gradient_c64", "qf_gradient_c64_ex", "qf_gradient_pergate_c64", "qf_plan_create",
+    "qf_plan_create_ex", "qf_plan_destroy",
     "qf_plan_upload_psi0", "qf_plan_set_psi0_device", "qf_plan_gradient",
     "qf_plan_gradient_device", "qf_plan_gradient_pergate", "qf_plan_forward_state",
     "qf_plan_stream", "qf_plan_synchronize", "qf_plan_traffic", "qf_plan_random_psi0", "qf_plan_download_psi0",
@@ -30,7 +31,10 @@ SYMBOLS = (
 )
 
 PROFILE_KINDS = ("forward_pass", "backward_pass", "observable", "resident", "prep_reduce",
-                 "pergate")
+                 "pergate", "slot_convert")
+# qfuse::StorageMode (engine.hpp:30)
+QF_STORAGE_FULL, QF_STORAGE_MEMSAVE = 0, 1
+STORAGE = {"full": QF_STORAGE_FULL, "memsave": QF_STORAGE_MEMSAVE}
 
 
 class QfError(RuntimeError):
@@ -88,8 +92,10 @@ def load(path: str = LIB_PATH):
                  C.POINTER(QfStats)]
     L.qf_gradient_c64.argtypes = grad_args
     L.qf_gradient_pergate_c64.argtypes = grad_args
+    L.qf_gradient_c64_ex.argtypes = grad_args[:7] + [C.c_uint32] + grad_args[7:]
     L.qf_plan_create.argtypes = [_P, _P, C.c_size_t, C.c_uint32, C.c_uint32, C.c_uint32,
                                  C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint64, C.POINTER(_P)]
+    L.qf_plan_create_ex.argtypes = L.qf_plan_create.argtypes[:-1] + [C.c_uint32, C.POINTER(_P)]
     L.qf_plan_destroy.argtypes = [_P]
     L.qf_plan_upload_psi0.argtypes = [_P, _P]
     L.qf_plan_set_psi0_device.argtypes = [_P, _P]
@@ -168,14 +174,15 @@ class Plan:
     """A planned circuit with its batch store resident in HBM."""
 
     def __init__(self, ctx: Context, gates, n_qubits: int, n_params: int, layers: int,
-                 ckpt_layers: int, batch: int, pauli):
+                 ckpt_layers: int, batch: int, pauli, storage: str = "full"):
         g = _gates(gates)
         self._gates = g
         self.ctx = ctx
         self.n, self.n_params, self.batch = n_qubits, n_params, batch
         h = _P()
-        _check(_lib.qf_plan_create(ctx.h, _ptr(g), len(g), n_qubits, n_params, layers,
-                                   ckpt_layers, batch, pauli[0], pauli[1], C.byref(h)))
+        _check(_lib.qf_plan_create_ex(ctx.h, _ptr(g), len(g), n_qubits, n_params, layers,
+                                      ckpt_layers, batch, pauli[0], pauli[1], STORAGE[storage],
+                                      C.byref(h)))
         self.h = h
 
     def upload_psi0(self, psi0):
@@ -253,8 +260,9 @@ class Plan:
 
 
 def gradient_c64(ctx: Context, gates, n_qubits, n_params, layers, ckpt_layers, psi0, theta,
-                 pauli, pergate: bool = False) -> GradientResult:
-    """One-shot qf_gradient_c64 (the reference's gradient<float>/run_checkpointed<float>)."""
+                 pauli, pergate: bool = False, storage: str = "full") -> GradientResult:
+    """One-shot qf_gradient_c64 (the reference's gradient<float>/run_checkpointed<float>);
+    storage "memsave" = StorageMode::MemSave (qf_gradient_c64_ex)."""
     g = _gates(gates)
     a = np.ascontiguousarray(psi0, np.float32)
     batch = a.shape[0]
@@ -263,6 +271,12 @@ def gradient_c64(ctx: Context, gates, n_qubits, n_params, layers, ckpt_layers, p
     exp = np.empty(batch, np.float64)
     loss = C.c_double()
     st = QfStats()
+    if storage != "full" and not pergate:
+        _check(_lib.qf_gradient_c64_ex(ctx.h, _ptr(g), len(g), n_qubits, n_params, layers,
+                                       ckpt_layers, STORAGE[storage], _ptr(a), batch, _ptr(th),
+                                       pauli[0], pauli[1], C.byref(loss), _ptr(grad), _ptr(exp),
+                                       C.byref(st)))
+        return GradientResult(loss.value, grad, exp, st.as_dict())
     fn = _lib.qf_gradient_pergate_c64 if pergate else _lib.qf_gradient_c64
     _check(fn(ctx.h, _ptr(g), len(g), n_qubits, n_params, layers, ckpt_layers, _ptr(a), batch,
               _ptr(th), pauli[0], pauli[1], C.byref(loss), _ptr(grad), _ptr(exp),

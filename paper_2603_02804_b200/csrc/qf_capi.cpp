@@ -139,6 +139,12 @@ struct qf_plan {
     size_t state_bytes = 0;
     // stores
     float2 *psi0 = nullptr, *W = nullptr, *lam = nullptr, *slots = nullptr;
+    // StorageMode::MemSave (streaming plans): checkpoint slots as bfloat16 pairs,
+    // the final state stays complex64 in W
+    uint32_t storage = QF_STORAGE_FULL;
+    uint32_t *slots16 = nullptr;
+    uint64_t device_bytes = 0; // batch store + slots + K partials
+    bool memsave() const { return storage == QF_STORAGE_MEMSAVE && !P.resident; }
     // theta-dependent stage data
     double *theta = nullptr, *out = nullptr;
     float2 *ry = nullptr;
@@ -249,13 +255,17 @@ void build_device_plan(qf_plan *pl) {
     const uint64_t tiles_res = pl->amps_padded / kTileAmps;
     pl->grid_res = int(std::min<uint64_t>(tiles_res, uint64_t(occ_r) * ctx->sms));
     const int grid_k = P.resident ? pl->grid_res : pl->grid_bwd;
-    const size_t n_states = P.resident ? (2 + P.n_slots) : (3 + P.n_slots);
+    // MemSave: slots hold bfloat16 pairs (half a state each); the last slot is
+    // the final state, kept complex64 in W
+    const size_t n_slot16 = pl->memsave() && P.n_slots > 0 ? P.n_slots - 1 : 0;
+    const size_t n_states = P.resident ? (2 + P.n_slots) : pl->memsave() ? 3 : (3 + P.n_slots);
     const size_t kpart_bytes = size_t(grid_k) * S * n * 8 * 8;
-    const size_t need = n_states * pl->state_bytes + kpart_bytes + size_t(S) * sizeof(DiagTab) +
-                        (size_t(64) << 20);
+    const size_t need = n_states * pl->state_bytes + n_slot16 * (pl->state_bytes / 2) + kpart_bytes +
+                        size_t(S) * sizeof(DiagTab) + (size_t(64) << 20);
     size_t free_b = 0, total_b = 0;
     ck(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
     const uint64_t budget = ctx->hbm_limit ? std::min<uint64_t>(ctx->hbm_limit, free_b) : free_b;
+    pl->device_bytes = need - (size_t(64) << 20);
     if (need > budget)
         throw CapacityError("device working set of " + std::to_string(need >> 20) +
                             " MiB (states + " + std::to_string(P.n_slots) +
@@ -267,7 +277,12 @@ void build_device_plan(qf_plan *pl) {
     ck(cudaMemset(pl->psi0, 0, pl->state_bytes), "memset");
     pl->lam = dalloc<float2>(pl->amps_padded, o);
     if (!P.resident) pl->W = dalloc<float2>(pl->amps_padded, o);
-    pl->slots = dalloc<float2>(size_t(pl->amps_padded) * std::max<uint32_t>(1, P.n_slots), o);
+    if (pl->memsave()) {
+        pl->slots = nullptr;
+        pl->slots16 = dalloc<uint32_t>(size_t(pl->amps_padded) * std::max<size_t>(1, n_slot16), o);
+    } else {
+        pl->slots = dalloc<float2>(size_t(pl->amps_padded) * std::max<uint32_t>(1, P.n_slots), o);
+    }
     pl->theta = dalloc<double>(P.n_params, o);
     pl->out = dalloc<double>(pl->out_len(), o);
     // stage data; ry defaults to identity, w to zero (entries no section writes)
@@ -315,8 +330,8 @@ void build_device_plan(qf_plan *pl) {
             pl->m_W.push_back(pass_map(pl->W, L, n, P.batch));
             pl->m_lam.push_back(pass_map(pl->lam, L, n, P.batch));
         }
-        pl->m_slot.resize(P.n_slots);
-        for (uint32_t j = 0; j < P.n_slots; ++j)
+        pl->m_slot.resize(pl->memsave() ? 0 : P.n_slots);
+        for (uint32_t j = 0; j < pl->m_slot.size(); ++j)
             for (const PassLayout &L : P.layouts)
                 pl->m_slot[j].push_back(pass_map(pl->slots + size_t(j) * pl->amps_padded, L, n, P.batch));
     }
@@ -421,15 +436,20 @@ void enqueue_fused(qf_plan *pl, const double *theta_dev, double *out_dev, qf_sta
         st.resident = 1;
     } else {
         const size_t NPS = P.steps.size();
-        const float2 *final_state = NPS ? pl->slots + size_t(P.n_slots - 1) * pl->amps_padded : pl->psi0;
-        // forward
+        const bool ms = pl->memsave();
+        const float2 *final_state = !NPS ? pl->psi0
+                                    : ms  ? pl->W
+                                          : pl->slots + size_t(P.n_slots - 1) * pl->amps_padded;
+        auto slot16 = [&](size_t pi) { return pl->slots16 + size_t(pi / P.ckpt_passes) * pl->amps_padded; };
+        // forward (MemSave: every pass in place on W; a slot pass is narrowed into its bf16 slot)
         for (size_t pi = 0; pi < NPS; ++pi) {
             const PassStep &ps = P.steps[pi];
             const CUtensorMap *in;
             if (pi == 0) in = &pl->m_psi0[ps.layout];
-            else if (P.slot_pass(pi - 1)) in = &pl->m_slot[(pi - 1) / P.ckpt_passes][ps.layout];
+            else if (!ms && P.slot_pass(pi - 1)) in = &pl->m_slot[(pi - 1) / P.ckpt_passes][ps.layout];
             else in = &pl->m_W[ps.layout];
-            const CUtensorMap *outm = P.slot_pass(pi) ? &pl->m_slot[pi / P.ckpt_passes][ps.layout] : &pl->m_W[ps.layout];
+            const CUtensorMap *outm = (!ms && P.slot_pass(pi)) ? &pl->m_slot[pi / P.ckpt_passes][ps.layout]
+                                                               : &pl->m_W[ps.layout];
             PassParams p = pass_params(pl, ps, true);
             pl->timed(0, 2 * sb, [&] {
                 ck(launch_pass(s, false, std::min(pl->grid_fwd, p.tiles), p, in, outm, nullptr), "pass fwd");
@@ -437,6 +457,11 @@ void enqueue_fused(qf_plan *pl, const double *theta_dev, double *out_dev, qf_sta
             st.kernel_launches++;
             st.forward_passes++;
             bytes += 2 * sb;
+            if (ms && P.slot_pass(pi) && pi + 1 < NPS && !forward_only) {
+                pl->timed(6, 1.5 * sb, [&] { ck(launch_narrow_bf16(s, pl->W, slot16(pi), pl->amps_padded), "narrow"); });
+                st.kernel_launches++;
+                bytes += 1.5 * sb;
+            }
         }
         SeedParams sp{};
         sp.n = int(n);
@@ -458,7 +483,14 @@ void enqueue_fused(qf_plan *pl, const double *theta_dev, double *out_dev, qf_sta
             for (size_t pi = NPS; pi-- > 0;) {
                 const PassStep &ps = P.steps[pi];
                 const bool from_slot = P.slot_pass(pi);
-                const CUtensorMap *in = from_slot ? &pl->m_slot[pi / P.ckpt_passes][ps.layout] : &pl->m_W[ps.layout];
+                const CUtensorMap *in = (from_slot && !ms) ? &pl->m_slot[pi / P.ckpt_passes][ps.layout]
+                                                           : &pl->m_W[ps.layout];
+                if (ms && from_slot && pi + 1 < NPS) { // re-anchor from the bf16 slot
+                    // (W is free: the pass after a slot pass did not write psi)
+                    pl->timed(6, 1.5 * sb, [&] { ck(launch_widen_bf16(s, slot16(pi), pl->W, pl->amps_padded), "widen"); });
+                    st.kernel_launches++;
+                    bytes += 1.5 * sb;
+                }
                 const bool write_psi = pi > 0 && !P.slot_pass(pi - 1);
                 PassParams p = pass_params(pl, ps, write_psi);
                 pl->timed(1, (write_psi ? 4 : 3) * sb, [&] {
@@ -555,10 +587,14 @@ void enqueue_pergate(qf_plan *pl, const double *theta_dev, double *out_dev, qf_s
 }
 
 qf_plan *create_plan(qf_ctx *ctx, const qf_gate *gates, size_t n_gates, uint32_t n, uint32_t n_params,
-                     uint32_t layers, uint32_t ckpt, uint32_t batch, uint64_t x, uint64_t z) {
+                     uint32_t layers, uint32_t ckpt, uint32_t batch, uint64_t x, uint64_t z,
+                     uint32_t storage = QF_STORAGE_FULL) {
     if (!ctx) throw std::invalid_argument("null context");
+    if (storage != QF_STORAGE_FULL && storage != QF_STORAGE_MEMSAVE)
+        throw std::invalid_argument("unknown storage mode");
     auto pl = std::make_unique<qf_plan>();
     pl->ctx = ctx;
+    pl->storage = storage;
     pl->P = make_plan(gates, n_gates, n, n_params, layers, ckpt, batch, x, z);
     build_device_plan(pl.get());
     return pl.release();
@@ -590,7 +626,7 @@ void run_host(qf_plan *pl, const double *theta, double *loss, double *grad, doub
     float ms = 0;
     cudaEventElapsedTime(&ms, pl->ev0, pl->ev1);
     st.device_ms = ms;
-    st.device_bytes = 0;
+    st.device_bytes = pl->device_bytes;
     *loss = pl->h_out[P.n_params];
     if (P.n_params) std::memcpy(grad, pl->h_out, sizeof(double) * P.n_params);
     if (expect) std::memcpy(expect, pl->h_out + P.n_params + 1, sizeof(double) * P.batch);
@@ -649,6 +685,16 @@ int qf_plan_create(qf_ctx *ctx, const qf_gate *gates, size_t n_gates, uint32_t n
         if (!out) throw std::invalid_argument("null output pointer");
         *out = create_plan(ctx, gates, n_gates, n_qubits, n_params, layers, ckpt_layers, batch,
                            x_mask, z_mask);
+    });
+}
+
+int qf_plan_create_ex(qf_ctx *ctx, const qf_gate *gates, size_t n_gates, uint32_t n_qubits,
+                      uint32_t n_params, uint32_t layers, uint32_t ckpt_layers, uint32_t batch,
+                      uint64_t x_mask, uint64_t z_mask, uint32_t storage_mode, qf_plan **out) {
+    return guarded([&] {
+        if (!out) throw std::invalid_argument("null output pointer");
+        *out = create_plan(ctx, gates, n_gates, n_qubits, n_params, layers, ckpt_layers, batch,
+                           x_mask, z_mask, storage_mode);
     });
 }
 
@@ -750,6 +796,20 @@ int qf_gradient_c64(qf_ctx *ctx, const qf_gate *gates, size_t n_gates, uint32_t 
         if (!psi0) throw std::invalid_argument("null psi0");
         std::unique_ptr<qf_plan> pl(create_plan(ctx, gates, n_gates, n_qubits, n_params, layers,
                                                 ckpt_layers, batch, x_mask, z_mask));
+        ck(cudaMemcpyAsync(pl->psi0, psi0, pl->amps * 8, cudaMemcpyHostToDevice, ctx->stream), "H2D psi0");
+        run_host(pl.get(), theta, loss_out, grad_out, expect_out, stats_out, Mode::Fused);
+    });
+}
+
+int qf_gradient_c64_ex(qf_ctx *ctx, const qf_gate *gates, size_t n_gates, uint32_t n_qubits,
+                       uint32_t n_params, uint32_t layers, uint32_t ckpt_layers,
+                       uint32_t storage_mode, const float *psi0, uint32_t batch,
+                       const double *theta, uint64_t x_mask, uint64_t z_mask, double *loss_out,
+                       double *grad_out, double *expect_out, qf_stats *stats_out) {
+    return guarded([&] {
+        if (!psi0) throw std::invalid_argument("null psi0");
+        std::unique_ptr<qf_plan> pl(create_plan(ctx, gates, n_gates, n_qubits, n_params, layers,
+                                                ckpt_layers, batch, x_mask, z_mask, storage_mode));
         ck(cudaMemcpyAsync(pl->psi0, psi0, pl->amps * 8, cudaMemcpyHostToDevice, ctx->stream), "H2D psi0");
         run_host(pl.get(), theta, loss_out, grad_out, expect_out, stats_out, Mode::Fused);
     });

@@ -146,6 +146,9 @@ cudaError_t launch_random_state(cudaStream_t st, uint64_t seed, uint64_t first_s
 // Z of every (stage >= 1, qubit) from the previous stage's (X, Z) and Ry angle
 // (qf_device.cuh kmeasure): streaming plans measure Z at stage 0 only.
 cudaError_t launch_zchain(cudaStream_t st, int stages, int n, const float2 *ry, double *kout);
+// StorageMode::MemSave slots: complex64 <-> bfloat16 pairs (uint32 per amplitude).
+cudaError_t launch_narrow_bf16(cudaStream_t st, const float2 *src, uint32_t *dst, uint64_t amps);
+cudaError_t launch_widen_bf16(cudaStream_t st, const uint32_t *src, float2 *dst, uint64_t amps);
 int pass_occupancy(bool backward);
 int resident_occupancy();
 size_t pass_smem_bytes(bool backward);

@@ -66,7 +66,8 @@ std::vector<qf_gate> to_gates(const std::vector<Gate> &gates) {
 GradientResult call(bool pergate, const std::vector<Gate> &flat, uint32_t n_qubits,
                     uint32_t n_params, uint32_t layers, uint32_t block_layers,
                     const BatchedState<float> &psi0, std::span<const double> theta,
-                    const PauliString &pauli, MemoryAccountant *accountant) {
+                    const PauliString &pauli, MemoryAccountant *accountant,
+                    StorageMode mode = StorageMode::Full) {
     if (psi0.n_qubits() != pauli.n_qubits)
         throw std::invalid_argument("engine: state qubit count mismatch"); // engine.cpp:438-442
     if (theta.size() != n_params)
@@ -75,25 +76,30 @@ GradientResult call(bool pergate, const std::vector<Gate> &flat, uint32_t n_qubi
     GradientResult r;
     r.gradient.assign(n_params, 0.0);
     qf_stats st{};
-    const auto fn = pergate ? qf_gradient_pergate_c64 : qf_gradient_c64;
-    check(fn(context(), gates.data(), gates.size(), n_qubits, n_params, layers, block_layers,
-             psi0.components().data(), psi0.batch(), theta.data(), pauli.x_mask, pauli.z_mask,
-             &r.loss, r.gradient.data(), nullptr, &st));
+    if (pergate) {
+        check(qf_gradient_pergate_c64(context(), gates.data(), gates.size(), n_qubits, n_params, layers,
+                                      block_layers, psi0.components().data(), psi0.batch(), theta.data(),
+                                      pauli.x_mask, pauli.z_mask, &r.loss, r.gradient.data(), nullptr, &st));
+    } else {
+        const uint32_t storage = mode == StorageMode::MemSave ? QF_STORAGE_MEMSAVE : QF_STORAGE_FULL;
+        check(qf_gradient_c64_ex(context(), gates.data(), gates.size(), n_qubits, n_params, layers,
+                                 block_layers, storage, psi0.components().data(), psi0.batch(),
+                                 theta.data(), pauli.x_mask, pauli.z_mask, &r.loss, r.gradient.data(),
+                                 nullptr, &st));
+    }
     r.stats.forward_traversals = st.forward_passes;
     r.stats.backward_traversals = st.backward_passes;
     r.stats.observable_traversals = st.observable_passes;
     // stored state vectors: checkpoint slots (+1 working store), in state units
-    r.stats.ledger_peak_units = st.resident ? 0.0 : double(st.stages ? st.stages / std::max(1u, st.ckpt_layers) + 1 : 1);
+    // (MemSave slots count half, accounting.hpp:25-61 / engine.hpp:47)
+    const double slots = st.stages ? double(st.stages / std::max(1u, st.ckpt_layers)) : 0.0;
+    r.stats.ledger_peak_units =
+        st.resident ? 0.0 : (mode == StorageMode::MemSave ? 0.5 * std::max(0.0, slots - 1) + 1.0 : slots + 1.0);
     if (accountant != nullptr) {
         accountant->add(r.stats.ledger_peak_units);
         accountant->release(r.stats.ledger_peak_units);
     }
     return r;
-}
-
-void reject_mem_save(StorageMode mode) {
-    if (mode == StorageMode::MemSave)
-        throw std::invalid_argument("qfuse-b200: StorageMode::MemSave is not supported yet");
 }
 
 } // namespace
@@ -103,22 +109,20 @@ void set_device(int device) { t_device = device; }
 GradientResult gradient(const FusedCircuit &fused, const BatchedState<float> &psi0,
                         std::span<const double> theta, const PauliString &pauli,
                         StorageMode mode, MemoryAccountant *accountant) {
-    reject_mem_save(mode);
     const auto flat = flatten(fused);
     return call(false, flat, fused.n_qubits, fused.n_params, 0, 0, psi0, theta, pauli,
-                accountant);
+                accountant, mode);
 }
 
 GradientResult run_checkpointed(const FusedCircuit &fused, const BatchedState<float> &psi0,
                                 std::span<const double> theta, const PauliString &pauli,
                                 const CheckpointPlan &plan, StorageMode mode,
                                 MemoryAccountant *accountant) {
-    reject_mem_save(mode);
     if (plan.ops_per_layer * plan.layers != fused.ops.size()) // checkpoint.cpp:149-151
         throw std::invalid_argument("run_checkpointed: plan does not cover the circuit");
     const auto flat = flatten(fused);
     return call(false, flat, fused.n_qubits, fused.n_params, plan.layers, plan.block_layers, psi0,
-                theta, pauli, accountant);
+                theta, pauli, accountant, mode);
 }
 
 GradientResult naive_gradient(const Circuit &circuit, const BatchedState<float> &psi0,

@@ -71,6 +71,19 @@ int main() {
         compare("16q run_checkpointed", b200::run_checkpointed(fused, psi0, theta, pauli, plan, StorageMode::Full),
                 run_checkpointed<float>(fused, psi0, theta, pauli, plan, StorageMode::Full));
     }
+    {   // StorageMode::MemSave against the reference's MemSave and its Full fp32
+        // gradient: acceptance C10 bound 5e-3 (acceptance.cpp:466-499)
+        Circuit c = build_hea(16, 4);
+        const auto theta = random_parameters(c.n_params(), 31);
+        const auto psi0 = new_random_state<float>(16, 2, 32);
+        const auto pauli = parse_pauli(repeated_ixyz_label(16));
+        const auto fused = fuse_circuit(c);
+        const auto plan = CheckpointPlan::uniform(fused.ops.size(), 4, 1);
+        const auto ours = b200::run_checkpointed(fused, psi0, theta, pauli, plan, StorageMode::MemSave);
+        const auto full = run_checkpointed<float>(fused, psi0, theta, pauli, plan, StorageMode::Full);
+        const double g = rel_diff(ours.gradient, full.gradient);
+        report("16q MemSave vs reference Full (C10 5e-3)", g <= 5e-3, g);
+    }
     {   // per-gate comparator: naive_gradient
         Circuit c = build_hea(5, 3);
         const auto theta = random_parameters(c.n_params(), 21);

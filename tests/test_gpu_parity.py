@@ -303,3 +303,52 @@ def test_config4_depth_fused_vs_pergate(ctx):
     assert err <= TOL, err
     assert rel_diff(fused.expect, pg.expect) <= TOL
     assert np.all(np.isfinite(fused.gradient))
+
+
+# ---- StorageMode::MemSave (bf16 checkpoint slots), acceptance C10 bound
+MEMSAVE_TOL = 5e-3  # acceptance.cpp:466-499 (bf16 storage vs fp32)
+
+
+@pytest.mark.parametrize("n,layers,batch,k", [(14, 6, 2, 1), (16, 8, 2, 2), (20, 4, 1, 1)])
+def test_memsave_matches_oracle(ctx, oracle, n, layers, batch, k):
+    gates, npar, theta, psi0, pauli = _hea_case(n, layers, batch, seed=900 + n)
+    ms = capi.gradient_c64(ctx, gates, n, npar, layers, k, psi0, theta, pauli, storage="memsave")
+    full = capi.gradient_c64(ctx, gates, n, npar, layers, k, psi0, theta, pauli)
+    ref = oracle.gradient(gates, n, npar, psi0, theta, pauli)
+    _check(full, ref)
+    _check(ms, ref, tol=MEMSAVE_TOL)
+    # the final state is complex64 either way: identical loss and expectations
+    assert ms.loss == full.loss
+    assert np.array_equal(ms.expect, full.expect)
+    # half-size slots: (n_slots - 1) bf16 slots instead of n_slots complex64 ones
+    assert ms.stats["device_bytes"] < full.stats["device_bytes"]
+
+
+def test_memsave_resident_is_full_precision(ctx):
+    gates, npar, theta, psi0, pauli = _hea_case(10, 6, 3, seed=31)
+    ms = capi.gradient_c64(ctx, gates, 10, npar, 6, 2, psi0, theta, pauli, storage="memsave")
+    full = capi.gradient_c64(ctx, gates, 10, npar, 6, 2, psi0, theta, pauli)
+    assert np.array_equal(ms.gradient, full.gradient) and ms.loss == full.loss
+
+
+def test_memsave_config4_depth(ctx):
+    """20q x 1000 layers, k = 10: bf16 re-anchoring every 10 layers stays within C10."""
+    n, layers, batch = 20, 1000, 2
+    gates, npar, theta, psi0, pauli = _hea_case(n, layers, batch, seed=4242)
+    full = capi.gradient_c64(ctx, gates, n, npar, layers, 10, psi0, theta, pauli)
+    ms = capi.gradient_c64(ctx, gates, n, npar, layers, 10, psi0, theta, pauli, storage="memsave")
+    err = rel_diff(ms.gradient, full.gradient)
+    assert err <= MEMSAVE_TOL, err
+    assert ms.stats["device_bytes"] < 0.7 * full.stats["device_bytes"]
+
+
+def test_memsave_plan_reuse(ctx):
+    """A MemSave plan reused across theta gives the one-shot result bit for bit."""
+    n, layers, batch = 16, 4, 2
+    gates, npar, theta, psi0, pauli = _hea_case(n, layers, batch, seed=8)
+    plan = capi.Plan(ctx, gates, n, npar, layers, 1, batch, pauli, storage="memsave")
+    plan.upload_psi0(psi0)
+    a = plan.gradient(theta)
+    b = plan.gradient(theta)
+    one = capi.gradient_c64(ctx, gates, n, npar, layers, 1, psi0, theta, pauli, storage="memsave")
+    assert np.array_equal(a.gradient, b.gradient) and np.array_equal(a.gradient, one.gradient)
