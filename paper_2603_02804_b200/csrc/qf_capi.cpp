@@ -513,13 +513,13 @@ void enqueue_fused(qf_plan *pl, const double *theta_dev, double *out_dev, qf_sta
                              P.resident ? nullptr : pl->epart, int(chunks), P.batch,
                              out_dev + P.n_params + 1),
                "reduce");
-            if (!P.resident) ck(launch_zchain(s, int(S), int(n), pl->ry, pl->kout), "zchain");
+            ck(launch_zchain(s, int(S), int(n), pl->ry, pl->kout), "zchain");
             ck(launch_finalize(s, int(P.sec_q.size()), pl->sec_q, pl->sec_stage, pl->sec_off,
                                pl->sec_gates, pl->sec_gamma, theta_dev, int(n), pl->kout, out_dev,
                                out_dev + P.n_params + 1, P.batch, out_dev + P.n_params),
                "finalize");
         });
-        st.kernel_launches += P.resident ? 2 : 3;
+        st.kernel_launches += 3;
     }
     st.hbm_bytes = uint64_t(bytes);
     st.ckpt_layers = P.ckpt_layers;

@@ -105,7 +105,8 @@ __global__ void __launch_bounds__(kThreads) seed_kernel(const SeedParams p) {
 constexpr size_t kResAcc = size_t(8) * 2 * 12 * 8 * sizeof(double);
 constexpr size_t res_smem() {
     return size_t(2) * kTileBytes + size_t(kTileAmps) * sizeof(double) + 64 +
-           2 * 24 * 16 /*rys*/ + 2 * 16 * 8 /*treg*/ + 2 * 6 * 8 /*mgs*/ + kResAcc + 1024;
+           2 * 24 * 16 /*rys*/ + 2 * 16 * 8 /*treg*/ + 2 * 6 * 8 /*mgs*/ + 64 /*kc, fold*/ + kResAcc +
+           1024;
 }
 
 __global__ void __launch_bounds__(kThreads, 2)
@@ -122,7 +123,9 @@ __global__ void __launch_bounds__(kThreads, 2)
     float4 *rys = reinterpret_cast<float4 *>(tail + 64);                  // [2 slots][24]
     float2 *treg_s = reinterpret_cast<float2 *>(tail + 64 + 2 * 24 * 16); // [2 slots][16]
     float2 *mgs = treg_s + 2 * 16;                                       // [2 slots][2][3]
-    double *acc = reinterpret_cast<double *>(tail + 64 + 2 * 24 * 16 + 2 * 16 * 8 + 2 * 6 * 8);
+    float *kc = reinterpret_cast<float *>(tail + 64 + 2 * 24 * 16 + 2 * 16 * 8 + 2 * 6 * 8); // [2][6]
+    int *fold = reinterpret_cast<int *>(kc + 12);                                          // [2]
+    double *acc = reinterpret_cast<double *>(tail + 64 + 2 * 24 * 16 + 2 * 16 * 8 + 2 * 6 * 8 + 64);
     const uint32_t tid = threadIdx.x, warp = tid >> 5;
     const int n = p.n, S = p.stages;
     const uint32_t rot = (n >= 12) ? 0xFFFu : ((1u << n) - 1u);
@@ -143,18 +146,38 @@ __global__ void __launch_bounds__(kThreads, 2)
     }
     __syncthreads();
     uint32_t phase = 0;
-    auto load_stage = [&](int s) { // stage data into slot s & 1 (threads 64..91)
+    // Stage data into slot s & 1 (threads 64..95). A stage is D_s then Ry_s on
+    // groups 0, 1, 2; when the product F of its group scales is >= 2^-40 the
+    // scales are folded into D_s (treg * F) and the Ry rounds run unscaled (the
+    // tile is off by f in (F, 1] until the stage ends); the backward's K
+    // measurements after undoing Ry_s on groups 2, 1, 0 then carry f^-2 and get
+    // kc = (M2)^2, (M2 M1)^2, F^2 (qf_pass.cu pass_prologue, same algebra).
+    auto load_stage = [&](int s) {
         const int sl = s & 1;
+        auto gscale = [&](int g) {
+            float M = 1.f;
+            for (int b = 0; b < 4; ++b)
+                if (4 * g + b < n) M *= ry_entry(p.ry[size_t(s) * n + 4 * g + b]).z;
+            return M;
+        };
         if (tid >= 64 && tid < 76) {
             const int lb = tid - 64;
             rys[sl * 24 + 12 + lb] = lb < n ? ry_entry(p.ry[size_t(s) * n + lb]) : make_float4(0.f, 0.f, 1.f, 0.f);
         } else if (tid >= 76 && tid < 92) {
-            treg_s[sl * 16 + (tid - 76)] = p.dt[s].treg[tid - 76];
+            const float M0 = gscale(0), M1 = gscale(1), M2 = gscale(2), F = M0 * M1 * M2;
+            float2 t = p.dt[s].treg[tid - 76];
+            if (F >= 0x1p-40f) t = make_float2(t.x * F, t.y * F);
+            treg_s[sl * 16 + (tid - 76)] = t;
+            if (tid == 76) {
+                const bool f = F >= 0x1p-40f;
+                fold[sl] = f;
+                kc[sl * 6 + 3 + 2] = f ? M2 * M2 : 1.f;
+                kc[sl * 6 + 3 + 1] = f ? (M2 * M1) * (M2 * M1) : 1.f;
+                kc[sl * 6 + 3 + 0] = f ? F * F : 1.f;
+            }
         } else if (tid >= 92 && tid < 95) { // round-1 group scales
             const int g = tid - 92;
-            float M = 1.f;
-            for (int b = 0; b < 4; ++b)
-                if (4 * g + b < n) M *= ry_entry(p.ry[size_t(s) * n + 4 * g + b]).z;
+            const float M = gscale(g);
             mgs[sl * 6 + 3 + g] = make_float2(M, M);
         }
     };
@@ -164,9 +187,9 @@ __global__ void __launch_bounds__(kThreads, 2)
         e.rys = rys + sl * 24;
         e.mgs = mgs + sl * 6;
         e.rot = rot;
-        e.scale = true;
-        e.kc = nullptr;
-        e.zm = 3u;
+        e.scale = !fold[sl];
+        e.kc = kc + sl * 6;
+        e.zm = s == 0 ? 3u : 0u; // Z at stage 0 only (zchain_kernel rebuilds the rest)
         e.treg_s = treg_s + sl * 16;
         e.acc_w = acc + warp * 2 * 12 * 8;
         const int c = p.stage_cz[s];
