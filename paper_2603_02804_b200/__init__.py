@@ -3,7 +3,7 @@ state-vector circuits (arXiv 2603.02804), behind a C-ABI drop-in for the
 reference qfuse engine. See include/qfuse_b200.h and DESIGN.md."""
 from . import circuits
 from .capi import (Context, GradientResult, Plan, QfCapacityError, QfError,
-                   QfInvalidArgument, gradient_c64, load, LIB_PATH, SYMBOLS)
+                   QfInvalidArgument, gradient_c64, gradient_c128, load, LIB_PATH, SYMBOLS)
 
-__all__ = ["circuits", "Context", "Plan", "GradientResult", "gradient_c64", "load",
+__all__ = ["circuits", "Context", "Plan", "GradientResult", "gradient_c64", "gradient_c128", "load",
            "QfError", "QfInvalidArgument", "QfCapacityError", "LIB_PATH", "SYMBOLS"]

@@ -165,4 +165,19 @@ cudaError_t launch_gate_grad_reduce(cudaStream_t st, const double *gpart, int gb
                                     const uint32_t *params, int n_rot, double *grad);
 int gate_grid(uint64_t pairs);
 
+// complex128 path (qf_c128.cu): per-gate fp64 kernels.
+int c128_gate_grid(uint64_t pairs);
+cudaError_t launch_gate_fwd_c128(cudaStream_t st, double2 *psi, int n, uint32_t batch, int kind,
+                                 int axis, uint32_t q0, uint32_t q1, const double *theta,
+                                 uint32_t param);
+cudaError_t launch_gate_bwd_c128(cudaStream_t st, double2 *psi, double2 *lam, int n, uint32_t batch,
+                                 int kind, int axis, uint32_t q0, uint32_t q1, const double *theta,
+                                 uint32_t param, double *gpart);
+cudaError_t launch_seed_c128(cudaStream_t st, int n, uint32_t batch, uint64_t x_mask, uint64_t z_mask,
+                             uint32_t y_count, const double2 *psi, double2 *lam, uint32_t chunks,
+                             double *epart);
+cudaError_t launch_reduce_c128(cudaStream_t st, const double *gpart, int gblocks,
+                               const uint32_t *params, int n_rot, double *grad, const double *epart,
+                               uint32_t chunks, uint32_t batch, double *expect, double *loss);
+
 } // namespace qfb

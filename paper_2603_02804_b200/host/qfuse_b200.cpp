@@ -102,9 +102,60 @@ GradientResult call(bool pergate, const std::vector<Gate> &flat, uint32_t n_qubi
     return r;
 }
 
+// complex128: every call runs the fp64 per-gate device path; MemSave has no
+// effect there (no slots are stored), as in the reference at double where
+// the narrowed type is float (statevec.hpp narrow_traits<double>).
+GradientResult call_c128(const std::vector<Gate> &flat, uint32_t n_qubits, uint32_t n_params,
+                         uint32_t layers, uint32_t block_layers, const BatchedState<double> &psi0,
+                         std::span<const double> theta, const PauliString &pauli,
+                         MemoryAccountant *accountant) {
+    if (psi0.n_qubits() != pauli.n_qubits)
+        throw std::invalid_argument("engine: state qubit count mismatch"); // engine.cpp:438-442
+    if (theta.size() != n_params)
+        throw std::invalid_argument("gradient: theta length mismatch"); // engine.cpp:721-723
+    const auto gates = to_gates(flat);
+    GradientResult r;
+    r.gradient.assign(n_params, 0.0);
+    qf_stats st{};
+    check(qf_gradient_c128(context(), gates.data(), gates.size(), n_qubits, n_params, layers,
+                           block_layers, psi0.components().data(), psi0.batch(), theta.data(),
+                           pauli.x_mask, pauli.z_mask, &r.loss, r.gradient.data(), nullptr, &st));
+    r.stats.forward_traversals = st.forward_passes;
+    r.stats.backward_traversals = st.backward_passes;
+    r.stats.observable_traversals = st.observable_passes;
+    r.stats.ledger_peak_units = 1.0; // the working store only
+    if (accountant != nullptr) {
+        accountant->add(r.stats.ledger_peak_units);
+        accountant->release(r.stats.ledger_peak_units);
+    }
+    return r;
+}
+
 } // namespace
 
 void set_device(int device) { t_device = device; }
+
+GradientResult gradient(const FusedCircuit &fused, const BatchedState<double> &psi0,
+                        std::span<const double> theta, const PauliString &pauli,
+                        StorageMode, MemoryAccountant *accountant) {
+    return call_c128(flatten(fused), fused.n_qubits, fused.n_params, 0, 0, psi0, theta, pauli, accountant);
+}
+
+GradientResult run_checkpointed(const FusedCircuit &fused, const BatchedState<double> &psi0,
+                                std::span<const double> theta, const PauliString &pauli,
+                                const CheckpointPlan &plan, StorageMode, MemoryAccountant *accountant) {
+    if (plan.ops_per_layer * plan.layers != fused.ops.size()) // checkpoint.cpp:149-151
+        throw std::invalid_argument("run_checkpointed: plan does not cover the circuit");
+    return call_c128(flatten(fused), fused.n_qubits, fused.n_params, plan.layers, plan.block_layers,
+                     psi0, theta, pauli, accountant);
+}
+
+GradientResult naive_gradient(const Circuit &circuit, const BatchedState<double> &psi0,
+                              std::span<const double> theta, const PauliString &pauli,
+                              MemoryAccountant *accountant) {
+    return call_c128(circuit.gates(), circuit.n_qubits(), circuit.n_params(), 0, 0, psi0, theta,
+                     pauli, accountant);
+}
 
 GradientResult gradient(const FusedCircuit &fused, const BatchedState<float> &psi0,
                         std::span<const double> theta, const PauliString &pauli,

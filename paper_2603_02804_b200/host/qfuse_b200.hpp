@@ -7,6 +7,8 @@
 //   qfuse::b200::gradient          <- qfuse::gradient<float>         engine.hpp:139-142
 //   qfuse::b200::run_checkpointed  <- qfuse::run_checkpointed<float> checkpoint.hpp:65-69
 //   qfuse::b200::naive_gradient    <- qfuse::naive_gradient<float>   engine.hpp:146-149
+//   and the BatchedState<double> overloads <- the <double> instantiations
+//   (engine.cpp:942, checkpoint.cpp:196-213), complex128 on the device.
 //
 // A caller switches by replacing `qfuse::gradient<float>(...)` with
 // `qfuse::b200::gradient(...)`. Errors are rethrown as the
@@ -38,6 +40,20 @@ GradientResult run_checkpointed(const FusedCircuit &fused, const BatchedState<fl
                                 MemoryAccountant *accountant = nullptr);
 
 GradientResult naive_gradient(const Circuit &circuit, const BatchedState<float> &psi0,
+                              std::span<const double> theta, const PauliString &pauli,
+                              MemoryAccountant *accountant = nullptr);
+
+// complex128 (the reference's double instantiations).
+GradientResult gradient(const FusedCircuit &fused, const BatchedState<double> &psi0,
+                        std::span<const double> theta, const PauliString &pauli,
+                        StorageMode mode, MemoryAccountant *accountant = nullptr);
+
+GradientResult run_checkpointed(const FusedCircuit &fused, const BatchedState<double> &psi0,
+                                std::span<const double> theta, const PauliString &pauli,
+                                const CheckpointPlan &plan, StorageMode mode,
+                                MemoryAccountant *accountant = nullptr);
+
+GradientResult naive_gradient(const Circuit &circuit, const BatchedState<double> &psi0,
                               std::span<const double> theta, const PauliString &pauli,
                               MemoryAccountant *accountant = nullptr);
 

@@ -84,6 +84,23 @@ int main() {
         const double g = rel_diff(ours.gradient, full.gradient);
         report("16q MemSave vs reference Full (C10 5e-3)", g <= 5e-3, g);
     }
+    {   // complex128: the reference's gradient<double> / run_checkpointed<double> at the
+        // double-precision bounds of acceptance C1/C8 (1e-10)
+        Circuit c = build_hea(6, 5);
+        const auto theta = random_parameters(c.n_params(), 41);
+        const auto psi0 = new_random_state<double>(6, 3, 42);
+        const auto pauli = parse_pauli(repeated_ixyz_label(6));
+        const auto fused = fuse_circuit(c);
+        const auto a = b200::gradient(fused, psi0, theta, pauli, StorageMode::Full);
+        const auto b = gradient<double>(fused, psi0, theta, pauli, StorageMode::Full);
+        const double g = std::max(rel_diff(a.gradient, b.gradient),
+                                  std::abs(a.loss - b.loss) / std::max(1.0, std::abs(b.loss)));
+        report("complex128 gradient<double> (1e-10)", g <= 1e-10, g);
+        const auto plan = CheckpointPlan::uniform(fused.ops.size(), 5, 1);
+        const auto cp = b200::run_checkpointed(fused, psi0, theta, pauli, plan, StorageMode::Full);
+        const double h = rel_diff(cp.gradient, b.gradient);
+        report("complex128 run_checkpointed<double> (1e-10)", h <= 1e-10, h);
+    }
     {   // per-gate comparator: naive_gradient
         Circuit c = build_hea(5, 3);
         const auto theta = random_parameters(c.n_params(), 21);

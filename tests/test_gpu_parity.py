@@ -352,3 +352,92 @@ def test_memsave_plan_reuse(ctx):
     b = plan.gradient(theta)
     one = capi.gradient_c64(ctx, gates, n, npar, layers, 1, psi0, theta, pauli, storage="memsave")
     assert np.array_equal(a.gradient, b.gradient) and np.array_equal(a.gradient, one.gradient)
+
+
+def test_memsave_against_reference_memsave(ctx, ref):
+    """Our MemSave (bf16 slots) and the reference's MemSave (bf16 ledger,
+    engine.cpp:488-530) on the same inputs: both within C10 of the fp32 Full result."""
+    n, layers, batch = 14, 4, 2
+    gates, npar, theta, psi0, pauli = _hea_case(n, layers, batch, seed=61)
+    _, g_full = ref.gradient(gates, n, npar, psi0, theta, pauli, layers=layers, block_layers=1)
+    _, g_ref_ms = ref.gradient(gates, n, npar, psi0, theta, pauli, layers=layers, block_layers=1,
+                               mode="mem_save")
+    ours = capi.gradient_c64(ctx, gates, n, npar, layers, 1, psi0, theta, pauli, storage="memsave")
+    assert rel_diff(g_ref_ms, g_full) <= MEMSAVE_TOL
+    assert rel_diff(ours.gradient, g_full) <= MEMSAVE_TOL
+
+
+# ---- complex128 (the reference's double instantiations): fp64 bounds of
+# acceptance C1/C2/C8 (1e-10, acceptance.cpp:113-170, :396-416)
+TOL64 = 1e-10
+
+
+def _check64(res, oracle_out):
+    loss, grad, exp = oracle_out
+    assert rel_diff(res.gradient, grad) <= TOL64, rel_diff(res.gradient, grad)
+    assert abs(res.loss - loss) <= TOL64 * max(abs(loss), float(np.sum(np.abs(exp))), 1e-300)
+    assert rel_diff(res.expect, exp) <= TOL64
+
+
+def test_c128_config1_golden(ctx, oracle):
+    gates, npar = C.build_hea(4, 4)
+    theta = C.random_parameters(npar, 1235)
+    psi0 = C.new_random_state(4, 8, 1234, np.float64)
+    pauli = C.parse_pauli(C.repeated_ixyz_label(4))
+    res = capi.gradient_c128(ctx, gates, 4, npar, 4, 0, psi0, theta, pauli)
+    assert abs(res.loss - (-0.583176427514288)) < 1e-13
+    assert abs(res.gradient.sum() - 3.42181987882572) < 1e-12
+    np.testing.assert_allclose(res.gradient[:4], [-0.280450334533137, -0.847963409542352,
+                                                  0.763083492874858, 0.369861766941313],
+                               atol=1e-13)
+    _check64(res, oracle.gradient(gates, 4, npar, psi0, theta, pauli))
+
+
+@pytest.mark.parametrize("n,ngates,seed", [(4, 40, 1), (6, 80, 2), (9, 60, 3), (13, 50, 4)])
+def test_c128_random_circuits(ctx, oracle, n, ngates, seed):
+    gates, npar = C.random_circuit(n, ngates, seed)
+    theta = C.random_parameters(npar, seed + 100)
+    psi0 = C.new_random_state(n, 3, seed + 200, np.float64)
+    pauli = C.parse_pauli(C.repeated_ixyz_label(n))
+    res = capi.gradient_c128(ctx, gates, n, npar, 0, 0, psi0, theta, pauli)
+    _check64(res, oracle.gradient(gates, n, npar, psi0, theta, pauli))
+
+
+@pytest.mark.parametrize("n,layers,batch", [(2, 3, 5), (12, 3, 2), (20, 2, 1)])
+def test_c128_hea(ctx, oracle, n, layers, batch):
+    gates, npar = C.build_hea(n, layers)
+    theta = C.random_parameters(npar, 7 + n)
+    psi0 = C.new_random_state(n, batch, 70 + n, np.float64)
+    pauli = C.parse_pauli(C.repeated_ixyz_label(n))
+    res = capi.gradient_c128(ctx, gates, n, npar, layers, 1, psi0, theta, pauli)
+    _check64(res, oracle.gradient(gates, n, npar, psi0, theta, pauli))
+
+
+def test_c128_against_reference_double(ctx, ref):
+    """The unmodified reference's gradient<double> on the same inputs."""
+    n, layers, batch = 8, 6, 4
+    gates, npar = C.build_hea(n, layers)
+    theta = C.random_parameters(npar, 22)
+    psi0 = C.new_random_state(n, batch, 21, np.float64)
+    pauli = C.parse_pauli(C.repeated_ixyz_label(n))
+    loss_r, grad_r = ref.gradient(gates, n, npar, psi0, theta, pauli, layers=layers)
+    res = capi.gradient_c128(ctx, gates, n, npar, layers, 0, psi0, theta, pauli)
+    assert rel_diff(res.gradient, grad_r) <= TOL64
+    assert abs(res.loss - loss_r) <= TOL64 * max(1.0, abs(loss_r))
+
+
+def test_c128_errors(ctx):
+    gates, npar = C.build_hea(4, 2)
+    psi0 = C.new_random_state(4, 2, 1, np.float64)
+    pauli = C.parse_pauli("IXYZ")
+    theta = C.random_parameters(npar, 2)
+    bad = gates.copy()
+    bad[0]["q0"] = 9
+    with pytest.raises(capi.QfInvalidArgument):
+        capi.gradient_c128(ctx, bad, 4, npar, 2, 0, psi0, theta, pauli)
+    bad = gates.copy()
+    bad[1]["param"] = 0  # parameter used twice
+    with pytest.raises(capi.QfInvalidArgument):
+        capi.gradient_c128(ctx, bad, 4, npar, 2, 0, psi0, theta, pauli)
+    with pytest.raises(capi.QfInvalidArgument):  # k does not divide layers
+        capi.gradient_c128(ctx, gates, 4, npar, 2, 3, psi0, theta, pauli)
