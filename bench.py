@@ -321,11 +321,11 @@ def run_ours(args):
     roofline["step_formula"] = f"B_U = S(6Pd + d/k + 1) with P={P} (BASELINE.md §2), our schedule moves P=1"
     # FP32 (CUDA-core) roofline of the dominant kernel: the paired-pass kernels are
     # FP32-bound. Algorithmic lane-FMA per amplitude per stage:
-    # forward 2n (one FFMA2 per output per qubit) + n/2 (group scales) + 8 (diag);
-    # backward 4n (Ry on psi and lambda) + 6n (X, Y, Z) + n (scales) + 16 (diag).
+    # forward 2n (one FFMA2 per output per qubit) + 8 (diag; group scales folded
+    # into it); backward 4n (Ry on psi and lambda) + 4n (X, Y; Z chained) + 16 (diag).
     fp = os.path.join(ROOT, "profiles", "fp32_peak.json")
     fp32_peak = json.load(open(fp))["tfma_per_s"] if os.path.exists(fp) else 36.9
-    per_amp = {"backward_pass": 11 * n + 16, "forward_pass": 2.5 * n + 8}.get(dom)
+    per_amp = {"backward_pass": 8 * n + 16, "forward_pass": 2 * n + 8}.get(dom)
     if per_amp and n > 12:
         stages_per_launch = layers / max(1, d["launches"] / max(1, args.steps))
         lane_fma = per_amp * B * (1 << n) * stages_per_launch
