@@ -389,6 +389,7 @@ PassParams pass_params(qf_plan *pl, const PassStep &ps, bool write_psi) {
     }
     p.write_psi = write_psi ? 1 : 0;
     p.zmask = (ps.s0 == 0 ? 1 : 0) | (ps.s1 == 0 ? 2 : 0);
+    p.prog = prog_encode(p.nph, p.ph, p.rot_mask);
     p.kpart = pl->kpart;
     p.kstride = (long long)P.stages * P.n * 8;
     return p;

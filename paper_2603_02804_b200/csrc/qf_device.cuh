@@ -395,7 +395,7 @@ __device__ __forceinline__ void phase_fwd(uint8_t *tile, uint32_t tau, const Pha
     if (OPS & 4u) ry_round<G, false, FULL>(v, e.rys + 12, e.rot, e.mgs[3 + G], e.scale);
     sts16<G>(tile, tau, v);
 }
-template <int G, uint32_t OPS, bool FULL>
+template <int G, uint32_t OPS, bool FULL, bool RTZ = true>
 __device__ __forceinline__ void phase_bwd(uint8_t *pt, uint8_t *lt, uint32_t tau, const PhaseEnv &e) {
     float2 p[16], l[16];
     lds16<G>(pt, tau, p);
@@ -403,7 +403,7 @@ __device__ __forceinline__ void phase_bwd(uint8_t *pt, uint8_t *lt, uint32_t tau
     if (OPS & 4u) {
         ry_round<G, true, FULL>(p, e.rys + 12, e.rot, e.mgs[3 + G], e.scale);
         ry_round<G, true, FULL>(l, e.rys + 12, e.rot, e.mgs[3 + G], e.scale);
-        if (e.zm & 2u) kmeasure<G, FULL, true>(p, l, e.rot, e.acc_w + 12 * 8, kcorr(e, 1, G));
+        if (RTZ && (e.zm & 2u)) kmeasure<G, FULL, true>(p, l, e.rot, e.acc_w + 12 * 8, kcorr(e, 1, G));
         else kmeasure<G, FULL, false>(p, l, e.rot, e.acc_w + 12 * 8, kcorr(e, 1, G));
     }
     if (OPS & 2u) {
@@ -413,7 +413,7 @@ __device__ __forceinline__ void phase_bwd(uint8_t *pt, uint8_t *lt, uint32_t tau
     if (OPS & 1u) {
         ry_round<G, true, FULL>(p, e.rys, e.rot, e.mgs[G], e.scale);
         ry_round<G, true, FULL>(l, e.rys, e.rot, e.mgs[G], e.scale);
-        if (e.zm & 1u) kmeasure<G, FULL, true>(p, l, e.rot, e.acc_w, kcorr(e, 0, G));
+        if (RTZ && (e.zm & 1u)) kmeasure<G, FULL, true>(p, l, e.rot, e.acc_w, kcorr(e, 0, G));
         else kmeasure<G, FULL, false>(p, l, e.rot, e.acc_w, kcorr(e, 0, G));
     }
     sts16<G>(pt, tau, p);
@@ -454,6 +454,42 @@ __device__ __forceinline__ void run_phase_bwd(int g, uint8_t *pt, uint8_t *lt, u
     if (g == 0) full ? run_bwd_g<0, true>(ops, pt, lt, tau, e) : run_bwd_g<0, false>(ops, pt, lt, tau, e);
     else if (g == 1) full ? run_bwd_g<1, true>(ops, pt, lt, tau, e) : run_bwd_g<1, false>(ops, pt, lt, tau, e);
     else full ? run_bwd_g<2, true>(ops, pt, lt, tau, e) : run_bwd_g<2, false>(ops, pt, lt, tau, e);
+}
+
+// ------------------------------------------------ compile-time phase programs
+// A pass's phase list as a constant, so the common passes (HEA interior passes
+// of layouts A and B) run as one straight-line sequence of inlined phases with
+// no runtime dispatch: bits 0..2 nph, bits 3..5 FULL per group, phase i at bit
+// 6 + 5i: group (2 bits), ops (3 bits). Encoded on the host by prog_encode.
+constexpr uint32_t prog_nph(uint32_t P) { return P & 7u; }
+constexpr bool prog_full(uint32_t P, int g) { return (P >> (3 + g)) & 1u; }
+constexpr int prog_g(uint32_t P, int i) { return int((P >> (6 + 5 * i)) & 3u); }
+constexpr uint32_t prog_ops(uint32_t P, int i) { return (P >> (8 + 5 * i)) & 7u; }
+
+// Backward: phases I, I-1, ..., 0 with SYNC() between them; no Z measurement.
+template <uint32_t P, int I, class Sync>
+__device__ __forceinline__ void prog_bwd(uint8_t *pt, uint8_t *lt, uint32_t tau, const PhaseEnv &e,
+                                         Sync &&sync) {
+    if constexpr (I >= 0) {
+        constexpr int g = prog_g(P, I);
+        phase_bwd<g, prog_ops(P, I), prog_full(P, g), false>(pt, lt, tau, e);
+        if constexpr (I > 0) {
+            sync();
+            prog_bwd<P, I - 1>(pt, lt, tau, e, sync);
+        }
+    }
+}
+// Forward: phases I, I+1, ..., nph-1.
+template <uint32_t P, int I, class Sync>
+__device__ __forceinline__ void prog_fwd(uint8_t *tile, uint32_t tau, const PhaseEnv &e, Sync &&sync) {
+    if constexpr (I < int(prog_nph(P))) {
+        constexpr int g = prog_g(P, I);
+        phase_fwd<g, prog_ops(P, I), prog_full(P, g)>(tile, tau, e);
+        if constexpr (I + 1 < int(prog_nph(P))) {
+            sync();
+            prog_fwd<P, I + 1>(tile, tau, e, sync);
+        }
+    }
 }
 
 } // namespace dev

@@ -62,6 +62,24 @@ struct PassPhase {
     int8_t g;
     uint8_t ops;
 };
+// Compile-time program of a pass (qf_device.cuh prog_*): 0 = none.
+constexpr uint32_t prog_encode(int nph, const PassPhase *ph, uint32_t rot_mask) {
+    uint32_t v = uint32_t(nph) & 7u;
+    for (int g = 0; g < 3; ++g)
+        if (((rot_mask >> (4 * g)) & 0xFu) == 0xFu) v |= 1u << (3 + g);
+    for (int i = 0; i < nph; ++i) v |= (uint32_t(ph[i].g) | (uint32_t(ph[i].ops) << 2)) << (6 + 5 * i);
+    return v;
+}
+// The programs compiled as straight-line kernels: interior passes of layout A
+// (12 rotated qubits, diagonal in group 0) and of layout B at n = 20 (groups
+// 1, 2) and n = 16 (group 2 only).
+constexpr PassPhase kProgAPh[5] = {{1, 1}, {2, 1}, {0, 7}, {1, 4}, {2, 4}};
+constexpr PassPhase kProgB20Ph[3] = {{1, 1}, {2, 7}, {1, 4}};
+constexpr PassPhase kProgB16Ph[1] = {{2, 7}};
+constexpr uint32_t kProgA = prog_encode(5, kProgAPh, 0xFFFu);
+constexpr uint32_t kProgB20 = prog_encode(3, kProgB20Ph, 0xFF0u);
+constexpr uint32_t kProgB16 = prog_encode(1, kProgB16Ph, 0xF00u);
+
 struct PassParams {
     int n;
     int tiles;
@@ -79,6 +97,7 @@ struct PassParams {
     const uint32_t *tileinfo;
     int write_psi;     // backward: store psi (0 when the next reader is a slot)
     int zmask;         // backward: bit r = round r measures Z (its stage is 0)
+    uint32_t prog;     // prog_encode(nph, ph, rot_mask)
     double *kpart;     // backward: [grid][stages][n][8]
     long long kstride; // stages*n*8
 };

@@ -80,7 +80,7 @@ constexpr size_t pass_smem(bool bwd, int nb) {
 }
 constexpr int min_blocks(bool bwd, int nb) { return bwd ? (nb == 1 ? 2 : 1) : 3; }
 
-template <bool BWD, int NB>
+template <bool BWD, int NB, uint32_t PROG = 0>
 __global__ void __launch_bounds__(kThreads, min_blocks(BWD, NB))
     pass_kernel(const __grid_constant__ PassParams p, const __grid_constant__ CUtensorMap m_in,
                 const __grid_constant__ CUtensorMap m_out,
@@ -140,7 +140,9 @@ __global__ void __launch_bounds__(kThreads, min_blocks(BWD, NB))
         if (p.dt) env.d = diag_ctx(tid, tthr, thrinfo, p.dt, p.cz, p.tileinfo, uint32_t(t) & tis_mask);
         mbar_wait(&mbar[b], (it / NB) & 1);
         uint8_t *pt = smem + b * kBuf;
-        if (!BWD) {
+        if (!BWD && PROG) {
+            prog_fwd<PROG, 0>(pt, tid, env, [] { __syncthreads(); });
+        } else if (!BWD) {
             for (int i = 0; i < p.nph; ++i) {
                 if (i) __syncthreads();
                 run_phase_fwd(p.ph[i].g, pt, tid, p.ph[i].ops, env);
@@ -197,6 +199,7 @@ __device__ __forceinline__ void named_bar(int id, int n) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
+template <uint32_t PROG = 0>
 __global__ void __launch_bounds__(kDualThreads, 1)
     pass_bwd_dual(const __grid_constant__ PassParams p, const __grid_constant__ CUtensorMap m_in,
                   const __grid_constant__ CUtensorMap m_out,
@@ -264,13 +267,24 @@ __global__ void __launch_bounds__(kDualThreads, 1)
         if (p.dt) env.d = diag_ctx(gtid, tthr, thrinfo, p.dt, p.cz, p.tileinfo, uint32_t(t) & tis_mask);
         mbar_wait(&mbar[k % 6], (k / 6) & 1);
         uint8_t *pt = smem + (k % 3) * kBuf;
-        for (int i = p.nph - 1; i >= 0; --i) {
-            if (i != p.nph - 1) named_bar(bar_id, kThreads);
-            run_phase_bwd(p.ph[i].g, pt, pt + kTileBytes, gtid, p.ph[i].ops, env);
-            if (i == p.nph - 1 && gtid == 0 && pending >= 0) {
+        auto refill = [&] {
+            if (gtid == 0 && pending >= 0) {
                 bulk_wait_read0();
                 issue_load(pending);
                 pending = -1;
+            }
+        };
+        if constexpr (PROG != 0) {
+            prog_bwd<PROG, int(prog_nph(PROG)) - 1>(pt, pt + kTileBytes, gtid, env, [&] {
+                refill();
+                named_bar(bar_id, kThreads);
+            });
+            refill(); // single-phase programs
+        } else {
+            for (int i = p.nph - 1; i >= 0; --i) {
+                if (i != p.nph - 1) named_bar(bar_id, kThreads);
+                run_phase_bwd(p.ph[i].g, pt, pt + kTileBytes, gtid, p.ph[i].ops, env);
+                if (i == p.nph - 1) refill();
             }
         }
         fence_async_smem();
@@ -317,21 +331,32 @@ int bwd_pipe() {
 }
 
 bool g_attrs = false;
+template <class K> cudaError_t set_smem(K kernel, size_t bytes) {
+    return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
+}
 cudaError_t ensure_attrs() {
     if (g_attrs) return cudaSuccess;
-    cudaError_t e = cudaFuncSetAttribute(pass_kernel<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int(pass_smem(false, 2)));
-    if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(pass_kernel<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 int(pass_smem(true, 1)));
-    if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(pass_kernel<true, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 int(pass_smem(true, 3)));
-    if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(pass_bwd_dual, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 int(dual_smem()));
+    cudaError_t e = set_smem(pass_kernel<false, 2>, pass_smem(false, 2));
+    if (e == cudaSuccess) e = set_smem(pass_kernel<false, 2, kProgA>, pass_smem(false, 2));
+    if (e == cudaSuccess) e = set_smem(pass_kernel<false, 2, kProgB20>, pass_smem(false, 2));
+    if (e == cudaSuccess) e = set_smem(pass_kernel<false, 2, kProgB16>, pass_smem(false, 2));
+    if (e == cudaSuccess) e = set_smem(pass_kernel<true, 1>, pass_smem(true, 1));
+    if (e == cudaSuccess) e = set_smem(pass_kernel<true, 3>, pass_smem(true, 3));
+    if (e == cudaSuccess) e = set_smem(pass_bwd_dual<0>, dual_smem());
+    if (e == cudaSuccess) e = set_smem(pass_bwd_dual<kProgA>, dual_smem());
+    if (e == cudaSuccess) e = set_smem(pass_bwd_dual<kProgB20>, dual_smem());
+    if (e == cudaSuccess) e = set_smem(pass_bwd_dual<kProgB16>, dual_smem());
     g_attrs = e == cudaSuccess;
     return e;
+}
+
+// QF_PROGS=0 forces the runtime-dispatch kernels (A/B timing).
+bool progs_enabled() {
+    static const bool v = [] {
+        const char *e = getenv("QF_PROGS");
+        return !e || atoi(e) != 0;
+    }();
+    return v;
 }
 
 } // namespace
@@ -349,7 +374,7 @@ int pass_occupancy(bool backward) {
     else if (bwd_pipe() == 3)
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, pass_kernel<true, 3>, kThreads, pass_smem(true, 3));
     else if (bwd_pipe() == 2)
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, pass_bwd_dual, kDualThreads, dual_smem());
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, pass_bwd_dual<0>, kDualThreads, dual_smem());
     else
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, pass_kernel<true, 1>, kThreads, pass_smem(true, 1));
     return blocks;
@@ -361,14 +386,26 @@ cudaError_t launch_pass(cudaStream_t st, bool backward, int grid, const PassPara
     cudaError_t e = ensure_attrs();
     if (e != cudaSuccess) return e;
     const CUtensorMap &l = lam ? *lam : *psi_out;
-    if (!backward)
-        pass_kernel<false, 2><<<grid, kThreads, pass_smem(false, 2), st>>>(p, *psi_in, *psi_out, l);
-    else if (bwd_pipe() == 3)
+    // straight-line kernels for the compiled programs (Z is measured at stage 0 only:
+    // those passes take the runtime-dispatch kernel)
+    const uint32_t prog = progs_enabled() && !(backward && p.zmask) ? p.prog : 0u;
+    if (!backward) {
+        const size_t sm = pass_smem(false, 2);
+        if (prog == kProgA) pass_kernel<false, 2, kProgA><<<grid, kThreads, sm, st>>>(p, *psi_in, *psi_out, l);
+        else if (prog == kProgB20) pass_kernel<false, 2, kProgB20><<<grid, kThreads, sm, st>>>(p, *psi_in, *psi_out, l);
+        else if (prog == kProgB16) pass_kernel<false, 2, kProgB16><<<grid, kThreads, sm, st>>>(p, *psi_in, *psi_out, l);
+        else pass_kernel<false, 2><<<grid, kThreads, sm, st>>>(p, *psi_in, *psi_out, l);
+    } else if (bwd_pipe() == 3) {
         pass_kernel<true, 3><<<grid, kThreads, pass_smem(true, 3), st>>>(p, *psi_in, *psi_out, l);
-    else if (bwd_pipe() == 2)
-        pass_bwd_dual<<<grid, kDualThreads, dual_smem(), st>>>(p, *psi_in, *psi_out, l);
-    else
+    } else if (bwd_pipe() == 2) {
+        const size_t sm = dual_smem();
+        if (prog == kProgA) pass_bwd_dual<kProgA><<<grid, kDualThreads, sm, st>>>(p, *psi_in, *psi_out, l);
+        else if (prog == kProgB20) pass_bwd_dual<kProgB20><<<grid, kDualThreads, sm, st>>>(p, *psi_in, *psi_out, l);
+        else if (prog == kProgB16) pass_bwd_dual<kProgB16><<<grid, kDualThreads, sm, st>>>(p, *psi_in, *psi_out, l);
+        else pass_bwd_dual<0><<<grid, kDualThreads, sm, st>>>(p, *psi_in, *psi_out, l);
+    } else {
         pass_kernel<true, 1><<<grid, kThreads, pass_smem(true, 1), st>>>(p, *psi_in, *psi_out, l);
+    }
     return cudaGetLastError();
 }
 

@@ -195,6 +195,18 @@ int main() {
         cudaEventElapsedTime(&ms, e0, e1);
         printf("mode bar, scales folded: %.3f ms  %.1f us/tile/half\n", ms, ms * 1e3 / iters);
     }
+    { // one half alone per SM (256 threads): how much do the two halves overlap?
+        cudaFuncSetAttribute(probe_var<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        for (int rep = 0; rep < 2; ++rep) {
+            cudaEventRecord(e0);
+            probe_var<1><<<148, 256, smem>>>(d, iters, o);
+            cudaEventRecord(e1);
+            cudaEventSynchronize(e1);
+            float ms;
+            cudaEventElapsedTime(&ms, e0, e1);
+            printf("one half per SM: %.1f us/tile\n", ms * 1e3 / iters);
+        }
+    }
     for (int m = 1; m <= 3; ++m) {
         if (m == 1) cudaFuncSetAttribute(probe_var<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
         if (m == 2) cudaFuncSetAttribute(probe_var<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
