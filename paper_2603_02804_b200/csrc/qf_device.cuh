@@ -12,6 +12,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 #include "qf_internal.h"
 
 namespace qfb {
@@ -466,7 +468,12 @@ constexpr bool prog_full(uint32_t P, int g) { return (P >> (3 + g)) & 1u; }
 constexpr int prog_g(uint32_t P, int i) { return int((P >> (6 + 5 * i)) & 3u); }
 constexpr uint32_t prog_ops(uint32_t P, int i) { return (P >> (8 + 5 * i)) & 7u; }
 
-// Backward: phases I, I-1, ..., 0 with SYNC() between them; no Z measurement.
+// Groups 0 and 1 place the same local bits (9..11) in the warp index (goff),
+// so between two such phases each warp reads only what it wrote: sync receives
+// std::integral_constant<bool, cross_warp> and may use __syncwarp.
+constexpr bool prog_cross(int ga, int gb) { return ga == 2 || gb == 2; }
+
+// Backward: phases I, I-1, ..., 0 with sync(cross) between them; no Z measurement.
 template <uint32_t P, int I, class Sync>
 __device__ __forceinline__ void prog_bwd(uint8_t *pt, uint8_t *lt, uint32_t tau, const PhaseEnv &e,
                                          Sync &&sync) {
@@ -474,7 +481,7 @@ __device__ __forceinline__ void prog_bwd(uint8_t *pt, uint8_t *lt, uint32_t tau,
         constexpr int g = prog_g(P, I);
         phase_bwd<g, prog_ops(P, I), prog_full(P, g), false>(pt, lt, tau, e);
         if constexpr (I > 0) {
-            sync();
+            sync(std::integral_constant<bool, prog_cross(g, prog_g(P, I - 1))>{});
             prog_bwd<P, I - 1>(pt, lt, tau, e, sync);
         }
     }
@@ -486,7 +493,7 @@ __device__ __forceinline__ void prog_fwd(uint8_t *tile, uint32_t tau, const Phas
         constexpr int g = prog_g(P, I);
         phase_fwd<g, prog_ops(P, I), prog_full(P, g)>(tile, tau, e);
         if constexpr (I + 1 < int(prog_nph(P))) {
-            sync();
+            sync(std::integral_constant<bool, prog_cross(g, prog_g(P, I + 1))>{});
             prog_fwd<P, I + 1>(tile, tau, e, sync);
         }
     }

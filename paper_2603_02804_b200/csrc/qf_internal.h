@@ -73,7 +73,7 @@ constexpr uint32_t prog_encode(int nph, const PassPhase *ph, uint32_t rot_mask) 
 // The programs compiled as straight-line kernels: interior passes of layout A
 // (12 rotated qubits, diagonal in group 0) and of layout B at n = 20 (groups
 // 1, 2) and n = 16 (group 2 only).
-constexpr PassPhase kProgAPh[5] = {{1, 1}, {2, 1}, {0, 7}, {1, 4}, {2, 4}};
+constexpr PassPhase kProgAPh[5] = {{2, 1}, {1, 1}, {0, 7}, {1, 4}, {2, 4}};
 constexpr PassPhase kProgB20Ph[3] = {{1, 1}, {2, 7}, {1, 4}};
 constexpr PassPhase kProgB16Ph[1] = {{2, 7}};
 constexpr uint32_t kProgA = prog_encode(5, kProgAPh, 0xFFFu);

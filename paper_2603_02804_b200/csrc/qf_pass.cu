@@ -141,7 +141,10 @@ __global__ void __launch_bounds__(kThreads, min_blocks(BWD, NB))
         mbar_wait(&mbar[b], (it / NB) & 1);
         uint8_t *pt = smem + b * kBuf;
         if (!BWD && PROG) {
-            prog_fwd<PROG, 0>(pt, tid, env, [] { __syncthreads(); });
+            prog_fwd<PROG, 0>(pt, tid, env, [](auto cross) {
+                if constexpr (decltype(cross)::value) __syncthreads();
+                else __syncwarp();
+            });
         } else if (!BWD) {
             for (int i = 0; i < p.nph; ++i) {
                 if (i) __syncthreads();
@@ -275,9 +278,10 @@ __global__ void __launch_bounds__(kDualThreads, 1)
             }
         };
         if constexpr (PROG != 0) {
-            prog_bwd<PROG, int(prog_nph(PROG)) - 1>(pt, pt + kTileBytes, gtid, env, [&] {
+            prog_bwd<PROG, int(prog_nph(PROG)) - 1>(pt, pt + kTileBytes, gtid, env, [&](auto cross) {
                 refill();
-                named_bar(bar_id, kThreads);
+                if constexpr (decltype(cross)::value) named_bar(bar_id, kThreads);
+                else __syncwarp();
             });
             refill(); // single-phase programs
         } else {

@@ -281,22 +281,28 @@ Plan make_plan(const qf_gate *gates, size_t n_gates, uint32_t n, uint32_t n_para
                 if (r[X] < S && dnext > r[X]) st.s1 = r[X]++;
             }
             // phases: round-0 groups (gd last), then round-1 groups
+            // Groups 0 and 1 share their warp bits (qf_device.cuh prog_cross): the
+            // round-0 group next to gd is its warp-bit partner, round 1 mirrored,
+            // so the compiled programs sync those transitions with __syncwarp.
             const PassLayout &L = plan.layouts[X];
             std::vector<int> groups;
             for (int g = 0; g < 3; ++g)
                 if (g != L.gd && (L.rot_mask >> (4 * g)) & 0xFu) groups.push_back(g);
+            auto partner = [](int a, int b) { return a != 2 && b != 2; };
+            if (groups.size() == 2 && partner(groups[0], L.gd) && !partner(groups[1], L.gd))
+                std::swap(groups[0], groups[1]);
             auto add = [&](int g, uint8_t ops) { st.ph[st.nph++] = PassPhase{int8_t(g), ops}; };
             const uint8_t d_op = st.sd >= 0 ? 2 : 0;
             const uint8_t gd_ops = uint8_t((st.s0 >= 0 ? 1 : 0) | d_op | (st.s1 >= 0 ? 4 : 0));
-            if (gd_ops == 1) { // round 0 only: any order; keep a row group last (direct epilogue)
+            if (gd_ops == 1) { // round 0 only: any order; gd first, then its partner
                 add(L.gd, 1);
-                for (int g : groups) add(g, 1);
+                for (auto it = groups.rbegin(); it != groups.rend(); ++it) add(*it, 1);
             } else {
                 if (st.s0 >= 0)
                     for (int g : groups) add(g, 1);
                 if (gd_ops) add(L.gd, gd_ops);
                 if (st.s1 >= 0)
-                    for (int g : groups) add(g, 4);
+                    for (auto it = groups.rbegin(); it != groups.rend(); ++it) add(*it, 4);
             }
             plan.steps.push_back(st);
             X = (X + 1) % NL;
