@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -390,6 +391,11 @@ PassParams pass_params(qf_plan *pl, const PassStep &ps, bool write_psi) {
     p.write_psi = write_psi ? 1 : 0;
     p.zmask = (ps.s0 == 0 ? 1 : 0) | (ps.s1 == 0 ? 2 : 0);
     p.prog = prog_encode(p.nph, p.ph, p.rot_mask);
+    static const int l2pf = [] {
+        const char *e = getenv("QF_L2PF");
+        return e ? atoi(e) : 1;
+    }();
+    p.l2pf = l2pf;
     p.kpart = pl->kpart;
     p.kstride = (long long)P.stages * P.n * 8;
     return p;

@@ -50,6 +50,14 @@ __device__ __forceinline__ void tma_load5(void *dst, const CUtensorMap *map, uin
                  "r"(c4), "r"(su32(bar))
                  : "memory");
 }
+// L2 prefetch of a 5-D tile (no shared memory, no completion tracking).
+__device__ __forceinline__ void tma_prefetch5(const CUtensorMap *map, int c0, int c1, int c2, int c3,
+                                              int c4) {
+    asm volatile("cp.async.bulk.prefetch.tensor.5d.L2.global.tile [%0, {%1, %2, %3, %4, %5}];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
+                 : "memory");
+}
 __device__ __forceinline__ void tma_store5(const CUtensorMap *map, const void *src, int c0, int c1,
                                            int c2, int c3, int c4) {
     asm volatile("cp.async.bulk.tensor.5d.global.shared::cta.bulk_group"
@@ -400,8 +408,18 @@ __device__ __forceinline__ void phase_fwd(uint8_t *tile, uint32_t tau, const Pha
 template <int G, uint32_t OPS, bool FULL, bool RTZ = true>
 __device__ __forceinline__ void phase_bwd(uint8_t *pt, uint8_t *lt, uint32_t tau, const PhaseEnv &e) {
     float2 p[16], l[16];
+#if QF_ABLATE_SMEM // timing ablation only: no shared-memory traffic in the phases
+#pragma unroll
+    for (int j = 0; j < 16; ++j) p[j] = l[j] = make_float2(float(tau + j), 1.f);
+#else
     lds16<G>(pt, tau, p);
     lds16<G>(lt, tau, l);
+#endif
+#if QF_ABLATE_MATH // timing ablation only: shared-memory traffic without the math
+    sts16<G>(pt, tau, p);
+    sts16<G>(lt, tau, l);
+    return;
+#endif
     if (OPS & 4u) {
         ry_round<G, true, FULL>(p, e.rys + 12, e.rot, e.mgs[3 + G], e.scale);
         ry_round<G, true, FULL>(l, e.rys + 12, e.rot, e.mgs[3 + G], e.scale);
@@ -418,8 +436,12 @@ __device__ __forceinline__ void phase_bwd(uint8_t *pt, uint8_t *lt, uint32_t tau
         if (RTZ && (e.zm & 1u)) kmeasure<G, FULL, true>(p, l, e.rot, e.acc_w, kcorr(e, 0, G));
         else kmeasure<G, FULL, false>(p, l, e.rot, e.acc_w, kcorr(e, 0, G));
     }
+#if QF_ABLATE_SMEM
+    if (p[0].x == 1.2345f && l[3].y == 5.4321f) sts16<G>(pt, tau, p); // keep the math live
+#else
     sts16<G>(pt, tau, p);
     sts16<G>(lt, tau, l);
+#endif
 }
 
 // Runtime (group, ops, full) -> template instance. ops in {1, 4, 2|4, 1|2|4}.

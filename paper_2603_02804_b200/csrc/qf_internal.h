@@ -98,6 +98,7 @@ struct PassParams {
     int write_psi;     // backward: store psi (0 when the next reader is a slot)
     int zmask;         // backward: bit r = round r measures Z (its stage is 0)
     uint32_t prog;     // prog_encode(nph, ph, rot_mask)
+    int l2pf;          // backward light passes: L2 prefetch of the next ring load
     double *kpart;     // backward: [grid][stages][n][8]
     long long kstride; // stages*n*8
 };

@@ -220,6 +220,9 @@ __global__ void __launch_bounds__(kDualThreads, 1)
     const uint32_t tid = threadIdx.x, warp = tid >> 5;
     const int half = int(tid >> 8);
     const uint32_t gtid = tid & 255u;
+    // light passes (layout B) are bound by the one-tile-deep ring: their next ring
+    // load is prefetched into L2 (QF_L2PF=0 disables)
+    const bool L2PF = PROG != 0 && prog_nph(PROG) <= 3 && p.l2pf;
 
     const int lo_mask = (1 << p.tile_lo_bits) - 1, hi_mask = (1 << p.tile_hi_bits) - 1;
     const int sample_shift = p.tile_lo_bits + p.tile_hi_bits;
@@ -268,6 +271,12 @@ __global__ void __launch_bounds__(kDualThreads, 1)
     for (int k = half; tile_of(k) < p.tiles; k += 2) {
         const int t = tile_of(k);
         if (p.dt) env.d = diag_ctx(gtid, tthr, thrinfo, p.dt, p.cz, p.tileinfo, uint32_t(t) & tis_mask);
+        if (L2PF && gtid == 0 && tile_of(k + 3) < p.tiles) { // the next ring load, into L2 now
+            const int tq = tile_of(k + 3);
+            const int c1 = tq & lo_mask, c3 = (tq >> p.tile_lo_bits) & hi_mask, c4 = tq >> sample_shift;
+            tma_prefetch5(&m_in, 0, c1, 0, c3, c4);
+            tma_prefetch5(&m_lam, 0, c1, 0, c3, c4);
+        }
         mbar_wait(&mbar[k % 6], (k / 6) & 1);
         uint8_t *pt = smem + (k % 3) * kBuf;
         auto refill = [&] {
@@ -277,6 +286,11 @@ __global__ void __launch_bounds__(kDualThreads, 1)
                 pending = -1;
             }
         };
+#if QF_ABLATE_PHASES
+        if (true) {
+            refill();
+        } else
+#endif
         if constexpr (PROG != 0) {
             prog_bwd<PROG, int(prog_nph(PROG)) - 1>(pt, pt + kTileBytes, gtid, env, [&](auto cross) {
                 refill();
