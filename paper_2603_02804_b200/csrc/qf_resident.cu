@@ -68,6 +68,14 @@ __device__ __forceinline__ float2 dfinal(uint32_t x, int n, const double *wf, co
 }
 
 // Streaming observable step (n > 12) / forward-state readout.
+// The seed factor 2 phase_O(t) D_f(t) conj(D_f(x)), t = x ^ X, factorises:
+//   angle(x) = sum_{q in X} (x_q ? -w_q : w_q) = W_X - 2 sum_{q in X, x_q = 1} w_q,
+//   CZ part  Q(x) ^ Q(x ^ X) = Q(X) ^ parity(x & M_X), M_X = xor of the adjacency
+//            rows of X (Q quadratic, so its difference is affine),
+// so a block (4096 amplitudes of one sample) builds e^{-2i w} products over the
+// low 6 + 6 bits of x in two 64-entry tables and one constant for its high bits:
+// per amplitude two table reads and two complex products instead of an fp64
+// sincos (and no per-amplitude loops).
 __global__ void __launch_bounds__(kThreads) seed_kernel(const SeedParams p) {
     const uint64_t dim = 1ull << p.n;
     const uint32_t per_block = dim < kTileAmps ? uint32_t(dim) : uint32_t(kTileAmps);
@@ -75,21 +83,71 @@ __global__ void __launch_bounds__(kThreads) seed_kernel(const SeedParams p) {
     const uint32_t s = blockIdx.x / chunks, chunk = blockIdx.x % chunks;
     const float2 *psi = p.psi + s * dim;
     float2 *lam = p.lam + s * dim;
+    if (p.apply_only) {
+        for (uint32_t k = threadIdx.x; k < per_block; k += kThreads) {
+            const uint32_t x = chunk * per_block + k;
+            lam[x] = cmul(dfinal(x, p.n, p.wfinal, p.czfinal), psi[x]);
+        }
+        return;
+    }
+    __shared__ float2 t_lo[64], t_mid[64];
+    __shared__ float2 c_blk;
+    __shared__ uint32_t m_x, q_x;
+    const uint32_t X = uint32_t(p.x_mask);
+    const uint32_t xb = chunk * per_block; // high bits of x (low 12 bits are k)
+    if (threadIdx.x < 128) {                // e^{-2i sum w} over bits 0..5 / 6..11 of x & X
+        const int sh = threadIdx.x < 64 ? 0 : 6;
+        const uint32_t v = (threadIdx.x & 63u) << sh;
+        double a = 0.0;
+        for (int q = sh; q < sh + 6 && q < p.n; ++q)
+            if (((v & X) >> q) & 1u) a += p.wfinal[q];
+        double sn, cs;
+        sincos(-2.0 * a, &sn, &cs);
+        (threadIdx.x < 64 ? t_lo : t_mid)[threadIdx.x & 63u] = make_float2(float(cs), float(sn));
+    } else if (threadIdx.x == 128) {        // 2 i^y e^{i (W_X - 2 sum over the block's high bits)}
+        double a = 0.0;
+        for (int q = 0; q < p.n; ++q)
+            if ((X >> q) & 1u) a += (q >= 12 && ((xb >> q) & 1u)) ? -p.wfinal[q] : p.wfinal[q];
+        double sn, cs;
+        sincos(a, &sn, &cs);
+        double re = 2.0 * cs, im = 2.0 * sn, r2 = re, i2 = im;
+        switch (p.y_count & 3u) {
+        case 1: r2 = -im; i2 = re; break;
+        case 2: r2 = -re; i2 = -im; break;
+        case 3: r2 = im; i2 = -re; break;
+        default: break;
+        }
+        c_blk = make_float2(float(r2), float(i2));
+    } else if (threadIdx.x == 160) {        // CZ difference: Q(X) and M_X
+        uint32_t m = 0, qx = 0;
+        if (p.czfinal) {
+            qx = qform_adj(p.czfinal, X);
+            for (int q = 0; q < p.n; ++q) {
+                if (!((X >> q) & 1u)) continue;
+                uint32_t row = p.czfinal->adjlo[q]; // neighbours p < q ...
+                for (int r = q + 1; r < p.n; ++r)   // ... and r > q
+                    if ((p.czfinal->adjlo[r] >> q) & 1u) row |= 1u << r;
+                m ^= row;
+            }
+        }
+        m_x = m;
+        q_x = qx;
+    }
+    __syncthreads();
+    const float2 cb = c_blk;
+    const uint32_t mx = m_x, qx = q_x, Z = uint32_t(p.z_mask);
     double e = 0.0;
     for (uint32_t k = threadIdx.x; k < per_block; k += kThreads) {
-        const uint32_t x = chunk * per_block + k;
-        if (p.apply_only) {
-            lam[x] = cmul(dfinal(x, p.n, p.wfinal, p.czfinal), psi[x]);
-            continue;
-        }
-        const uint32_t t = x ^ uint32_t(p.x_mask);
-        const float2 f = seed_factor(x, p.x_mask, p.z_mask, p.y_count, p.wfinal, p.czfinal);
+        const uint32_t x = xb + k, t = x ^ X;
+        const uint32_t par = (__popc(t & Z) + qx + __popc(x & mx)) & 1u;
+        const uint32_t xl = x & X;
+        float2 f = cmul(cb, cmul(t_lo[xl & 63u], t_mid[(xl >> 6) & 63u]));
+        if (par) f = make_float2(-f.x, -f.y);
         const float2 pt = psi[t], px = psi[x];
         const float2 l = cmul(f, pt);
         lam[x] = l;
         e += 0.5 * (double(px.x) * double(l.x) + double(px.y) * double(l.y));
     }
-    if (p.apply_only) return;
     __shared__ double red[kThreads / 32];
 #pragma unroll
     for (int m = 16; m >= 1; m >>= 1) e += __shfl_xor_sync(0xffffffffu, e, m);
