@@ -11,7 +11,7 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
   > gpurun_out/launches_${TAG}.log 2>&1; echo "launch list rc=$?"
 for K in bwd:pass_bwd_dual fwd:pass_kernel; do
   timeout 400 ncu --set full --clock-control none --import-source on -k regex:${K#*:} \
-    --launch-skip 5 -c 1 -o gpurun_out/prof_${K%%:*}_${TAG} -f \
+    --launch-skip 6 -c 2 -o gpurun_out/prof_${K%%:*}_${TAG} -f \
     python bench.py --steps 1 --warmup 0 --no-cpu --layers 20 "$@" \
     > gpurun_out/prof_${K%%:*}_${TAG}.log 2>&1; echo "ncu ${K%%:*} rc=$?"
 done
