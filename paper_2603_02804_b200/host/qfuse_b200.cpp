@@ -176,6 +176,24 @@ GradientResult run_checkpointed(const FusedCircuit &fused, const BatchedState<fl
                 theta, pauli, accountant, mode);
 }
 
+GradientResult run_checkpointed_naive(const Circuit &circuit, const BatchedState<float> &psi0,
+                                      std::span<const double> theta, const PauliString &pauli,
+                                      const CheckpointPlan &plan, MemoryAccountant *accountant) {
+    if (plan.ops_per_layer * plan.layers != circuit.gates().size()) // checkpoint.cpp:172-175
+        throw std::invalid_argument("run_checkpointed_naive: plan does not cover the circuit");
+    return call(true, circuit.gates(), circuit.n_qubits(), circuit.n_params(), plan.layers,
+                plan.block_layers, psi0, theta, pauli, accountant);
+}
+
+GradientResult run_checkpointed_naive(const Circuit &circuit, const BatchedState<double> &psi0,
+                                      std::span<const double> theta, const PauliString &pauli,
+                                      const CheckpointPlan &plan, MemoryAccountant *accountant) {
+    if (plan.ops_per_layer * plan.layers != circuit.gates().size())
+        throw std::invalid_argument("run_checkpointed_naive: plan does not cover the circuit");
+    return call_c128(circuit.gates(), circuit.n_qubits(), circuit.n_params(), plan.layers,
+                     plan.block_layers, psi0, theta, pauli, accountant);
+}
+
 GradientResult naive_gradient(const Circuit &circuit, const BatchedState<float> &psi0,
                               std::span<const double> theta, const PauliString &pauli,
                               MemoryAccountant *accountant) {

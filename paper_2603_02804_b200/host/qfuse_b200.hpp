@@ -7,6 +7,7 @@
 //   qfuse::b200::gradient          <- qfuse::gradient<float>         engine.hpp:139-142
 //   qfuse::b200::run_checkpointed  <- qfuse::run_checkpointed<float> checkpoint.hpp:65-69
 //   qfuse::b200::naive_gradient    <- qfuse::naive_gradient<float>   engine.hpp:146-149
+//   qfuse::b200::run_checkpointed_naive <- run_checkpointed_naive<float> checkpoint.hpp:73-79
 //   and the BatchedState<double> overloads <- the <double> instantiations
 //   (engine.cpp:942, checkpoint.cpp:196-213), complex128 on the device.
 //
@@ -43,6 +44,11 @@ GradientResult naive_gradient(const Circuit &circuit, const BatchedState<float> 
                               std::span<const double> theta, const PauliString &pauli,
                               MemoryAccountant *accountant = nullptr);
 
+GradientResult run_checkpointed_naive(const Circuit &circuit, const BatchedState<float> &psi0,
+                                      std::span<const double> theta, const PauliString &pauli,
+                                      const CheckpointPlan &plan,
+                                      MemoryAccountant *accountant = nullptr);
+
 // complex128 (the reference's double instantiations).
 GradientResult gradient(const FusedCircuit &fused, const BatchedState<double> &psi0,
                         std::span<const double> theta, const PauliString &pauli,
@@ -56,5 +62,10 @@ GradientResult run_checkpointed(const FusedCircuit &fused, const BatchedState<do
 GradientResult naive_gradient(const Circuit &circuit, const BatchedState<double> &psi0,
                               std::span<const double> theta, const PauliString &pauli,
                               MemoryAccountant *accountant = nullptr);
+
+GradientResult run_checkpointed_naive(const Circuit &circuit, const BatchedState<double> &psi0,
+                                      std::span<const double> theta, const PauliString &pauli,
+                                      const CheckpointPlan &plan,
+                                      MemoryAccountant *accountant = nullptr);
 
 } // namespace qfuse::b200

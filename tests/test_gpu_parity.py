@@ -441,3 +441,27 @@ def test_c128_errors(ctx):
         capi.gradient_c128(ctx, bad, 4, npar, 2, 0, psi0, theta, pauli)
     with pytest.raises(capi.QfInvalidArgument):  # k does not divide layers
         capi.gradient_c128(ctx, gates, 4, npar, 2, 3, psi0, theta, pauli)
+
+
+def test_cpp_bench_driver():
+    """qfuse::b200::run_bench / scan_blocks (the reference's bench API on the B200)
+    against the reference's run_bench on the same BenchConfig; the reference's
+    JSON/CSV serialisers round-trip our BenchReport; the CLI prints its JSON."""
+    import json
+    import os
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = os.path.join(root, "build", "tests", "bench_driver")
+    if not os.path.exists(exe):
+        pytest.skip("build/tests/bench_driver not built (needs the reference sources at build time)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=900)
+    print(r.stdout)
+    assert r.returncode == 0 and "ALL PASSED" in r.stdout, r.stdout + r.stderr
+    r = subprocess.run([exe, "--qubits", "16", "--layers", "20", "--batch", "8", "--block", "10",
+                        "--reps", "2", "--warmup", "1"], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr
+    rep = json.loads(r.stdout)
+    assert rep["config"]["qubits"] == 16 and rep["results"]["throughput_sps"] > 0
+    r = subprocess.run([exe, "--qubits", "4", "--layers", "3", "--block", "2"],
+                       capture_output=True, text=True, timeout=60)
+    assert r.returncode == 2  # config error exit code (qfuse_bench_main.cpp:110-116)
