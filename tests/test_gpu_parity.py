@@ -465,3 +465,23 @@ def test_cpp_bench_driver():
     r = subprocess.run([exe, "--qubits", "4", "--layers", "3", "--block", "2"],
                        capture_output=True, text=True, timeout=60)
     assert r.returncode == 2  # config error exit code (qfuse_bench_main.cpp:110-116)
+
+
+def test_config3_depth_subset_vs_oracle(ctx, oracle):
+    """BASELINE config 3 shape (16q x 200 layers, k = 10) on a 2-sample subset of
+    the batch against the fp64 oracle: the compiled layout-A/B programs, the Z
+    chain over 200 stages and the re-anchoring, at the stated 1e-4."""
+    n, layers, batch = 16, 200, 2
+    gates, npar, theta, psi0, pauli = _hea_case(n, layers, batch, seed=1234)
+    res = capi.gradient_c64(ctx, gates, n, npar, layers, 10, psi0, theta, pauli)
+    _check(res, oracle.gradient(gates, n, npar, psi0, theta, pauli))
+
+
+def test_config4_shape_vs_oracle(ctx, oracle):
+    """BASELINE config 4 register (20 qubits) at 40 layers, k = 10, one sample,
+    against the fp64 oracle (the full 1000 layers are cross-checked against the
+    per-gate path in test_config4_depth_fused_vs_pergate)."""
+    n, layers, batch = 20, 40, 1
+    gates, npar, theta, psi0, pauli = _hea_case(n, layers, batch, seed=1234)
+    res = capi.gradient_c64(ctx, gates, n, npar, layers, 10, psi0, theta, pauli)
+    _check(res, oracle.gradient(gates, n, npar, psi0, theta, pauli))
