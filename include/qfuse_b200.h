@@ -184,6 +184,47 @@ typedef struct qf_profile {
 } qf_profile;
 int qf_plan_set_profiling(qf_plan *plan, int enable);
 int qf_plan_profile(qf_plan *plan, qf_profile *out, int reset);
+/* Counters of the plan's last gradient (qf_plan_gradient* / _device). */
+int qf_plan_last_stats(const qf_plan *plan, qf_stats *out);
+
+/* ---- multi-GPU, one process ----
+ * Samples are independent and loss/gradient are sums over samples
+ * (engine.cpp:733-738, :686-689): device i of the group owns the contiguous
+ * sample range [i*B/G + min(i, B%G), ...) (sizes differ by at most one), runs
+ * the whole fused gradient on its shard, and the only exchange is one
+ * ncclAllReduce(sum, fp64) of [grad | loss] (n_params + 1 doubles) across the
+ * group over NVLink. NCCL is loaded at qf_group_create (libnccl.so.2); if it
+ * is missing the call fails with QF_EDEVICE. A multi-process job (one rank per
+ * GPU, torchrun) uses qf_plan_gradient_device + its own all-reduce instead.
+ * expect_out receives every sample's <O> in global order. stats_out sums the
+ * counters over devices; device_ms is the max over devices. */
+typedef struct qf_group qf_group;
+typedef struct qf_group_plan qf_group_plan;
+/* devices: n_gpus distinct CUDA ordinals, or NULL for 0..n_gpus-1. */
+int qf_group_create(int n_gpus, const int *devices, qf_group **out);
+int qf_group_destroy(qf_group *group);
+int qf_group_size(const qf_group *group);
+/* Plans the circuit once on every device for `batch` global samples. */
+int qf_group_plan_create(qf_group *group, const qf_gate *gates, size_t n_gates,
+                         uint32_t n_qubits, uint32_t n_params, uint32_t layers,
+                         uint32_t ckpt_layers, uint32_t batch, uint64_t x_mask, uint64_t z_mask,
+                         uint32_t storage_mode, qf_group_plan **out);
+int qf_group_plan_destroy(qf_group_plan *gplan);
+/* psi0_host: the whole batch (batch*2^(n+1) floats); each device copies its shard. */
+int qf_group_plan_upload_psi0(qf_group_plan *gplan, const float *psi0_host);
+/* new_random_state<float>(n, batch, seed) on the devices (global sample order). */
+int qf_group_plan_random_psi0(qf_group_plan *gplan, uint64_t seed);
+int qf_group_plan_gradient(qf_group_plan *gplan, const double *theta, double *loss_out,
+                           double *grad_out, double *expect_out, qf_stats *stats_out);
+/* The one-shot multi-GPU call (the reference's gradient<float> /
+ * run_checkpointed<float> over n_gpus devices). The group for a device list is
+ * created on first use and kept for the life of the process. */
+int qf_gradient_c64_multi(int n_gpus, const int *devices, const qf_gate *gates, size_t n_gates,
+                          uint32_t n_qubits, uint32_t n_params, uint32_t layers,
+                          uint32_t ckpt_layers, uint32_t storage_mode, const float *psi0,
+                          uint32_t batch, const double *theta, uint64_t x_mask, uint64_t z_mask,
+                          double *loss_out, double *grad_out, double *expect_out,
+                          qf_stats *stats_out);
 
 #ifdef __cplusplus
 }

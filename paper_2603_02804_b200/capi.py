@@ -28,7 +28,10 @@ SYMBOLS = (
     "qf_plan_upload_psi0", "qf_plan_set_psi0_device", "qf_plan_gradient",
     "qf_plan_gradient_device", "qf_plan_gradient_pergate", "qf_plan_forward_state",
     "qf_plan_stream", "qf_plan_synchronize", "qf_plan_traffic", "qf_plan_random_psi0", "qf_plan_download_psi0",
-    "qf_plan_set_profiling", "qf_plan_profile",
+    "qf_plan_set_profiling", "qf_plan_profile", "qf_plan_last_stats",
+    "qf_group_create", "qf_group_destroy", "qf_group_size", "qf_group_plan_create",
+    "qf_group_plan_destroy", "qf_group_plan_upload_psi0", "qf_group_plan_random_psi0",
+    "qf_group_plan_gradient", "qf_gradient_c64_multi",
 )
 
 PROFILE_KINDS = ("forward_pass", "backward_pass", "observable", "resident", "prep_reduce",
@@ -114,6 +117,19 @@ def load(path: str = LIB_PATH):
     L.qf_plan_download_psi0.argtypes = [_P, _P]
     L.qf_plan_set_profiling.argtypes = [_P, C.c_int]
     L.qf_plan_profile.argtypes = [_P, C.POINTER(QfProfile), C.c_int]
+    L.qf_plan_last_stats.argtypes = [_P, C.POINTER(QfStats)]
+    L.qf_group_create.argtypes = [C.c_int, _P, C.POINTER(_P)]
+    L.qf_group_destroy.argtypes = [_P]
+    L.qf_group_size.argtypes = [_P]
+    L.qf_group_plan_create.argtypes = [_P, _P, C.c_size_t, C.c_uint32, C.c_uint32, C.c_uint32,
+                                       C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint64,
+                                       C.c_uint32, C.POINTER(_P)]
+    L.qf_group_plan_destroy.argtypes = [_P]
+    L.qf_group_plan_upload_psi0.argtypes = [_P, _P]
+    L.qf_group_plan_random_psi0.argtypes = [_P, C.c_uint64]
+    L.qf_group_plan_gradient.argtypes = L.qf_plan_gradient.argtypes
+    L.qf_gradient_c64_multi.argtypes = ([C.c_int, _P] + grad_args[1:7] + [C.c_uint32]
+                                        + grad_args[7:])
     _lib = L
     return L
 
@@ -300,4 +316,102 @@ def gradient_c128(ctx: Context, gates, n_qubits, n_params, layers, ckpt_layers, 
     _check(_lib.qf_gradient_c128(ctx.h, _ptr(g), len(g), n_qubits, n_params, layers, ckpt_layers,
                                  _ptr(a), batch, _ptr(th), pauli[0], pauli[1], C.byref(loss),
                                  _ptr(grad), _ptr(exp), C.byref(st)))
+    return GradientResult(loss.value, grad, exp, st.as_dict())
+
+
+def _devices(devices):
+    if devices is None:
+        return None, None
+    arr = (C.c_int * len(devices))(*devices)
+    return arr, C.cast(arr, C.c_void_p)
+
+
+class Group:
+    """qf_group: one process driving several devices of the box, one NCCL
+    all-reduce of [grad | loss] per gradient (include/qfuse_b200.h)."""
+
+    def __init__(self, n_gpus: int, devices=None):
+        L = load()
+        keep, dp = _devices(devices)
+        h = _P()
+        _check(L.qf_group_create(n_gpus, dp, C.byref(h)))
+        self.h = h
+        self.size = L.qf_group_size(h)
+
+    def close(self):
+        if getattr(self, "h", None):
+            _lib.qf_group_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class GroupPlan:
+    """qf_group_plan: a planned circuit over a group, the batch sharded in order."""
+
+    def __init__(self, group: Group, gates, n_qubits: int, n_params: int, layers: int,
+                 ckpt_layers: int, batch: int, pauli, storage: str = "full"):
+        g = _gates(gates)
+        self.group = group
+        self.n, self.n_params, self.batch = n_qubits, n_params, batch
+        h = _P()
+        _check(_lib.qf_group_plan_create(group.h, _ptr(g), len(g), n_qubits, n_params, layers,
+                                         ckpt_layers, batch, pauli[0], pauli[1], STORAGE[storage],
+                                         C.byref(h)))
+        self.h = h
+
+    def upload_psi0(self, psi0):
+        a = np.ascontiguousarray(psi0, np.float32)
+        if a.size != self.batch * (2 << self.n):
+            raise ValueError("psi0 shape does not match the plan")
+        _check(_lib.qf_group_plan_upload_psi0(self.h, _ptr(a)))
+
+    def random_psi0(self, seed: int):
+        _check(_lib.qf_group_plan_random_psi0(self.h, seed))
+
+    def gradient(self, theta) -> GradientResult:
+        th = np.ascontiguousarray(theta, np.float64)
+        if th.size != self.n_params:
+            raise QfInvalidArgument(QF_EINVAL, "gradient: theta length mismatch")
+        grad = np.empty(self.n_params, np.float64)
+        exp = np.empty(self.batch, np.float64)
+        loss = C.c_double()
+        st = QfStats()
+        _check(_lib.qf_group_plan_gradient(self.h, _ptr(th), C.byref(loss), _ptr(grad), _ptr(exp),
+                                           C.byref(st)))
+        return GradientResult(loss.value, grad, exp, st.as_dict())
+
+    def close(self):
+        if getattr(self, "h", None):
+            _lib.qf_group_plan_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def gradient_c64_multi(n_gpus: int, gates, n_qubits, n_params, layers, ckpt_layers, psi0, theta,
+                       pauli, devices=None, storage: str = "full") -> GradientResult:
+    """One-shot qf_gradient_c64_multi: the batch sharded over n_gpus devices."""
+    load()
+    g = _gates(gates)
+    a = np.ascontiguousarray(psi0, np.float32)
+    batch = a.shape[0]
+    th = np.ascontiguousarray(theta, np.float64)
+    grad = np.empty(n_params, np.float64)
+    exp = np.empty(batch, np.float64)
+    loss = C.c_double()
+    st = QfStats()
+    keep, dp = _devices(devices)
+    _check(_lib.qf_gradient_c64_multi(n_gpus, dp, _ptr(g), len(g), n_qubits, n_params, layers,
+                                      ckpt_layers, STORAGE[storage], _ptr(a), batch, _ptr(th),
+                                      pauli[0], pauli[1], C.byref(loss), _ptr(grad), _ptr(exp),
+                                      C.byref(st)))
     return GradientResult(loss.value, grad, exp, st.as_dict())

@@ -752,6 +752,7 @@ int qf_plan_gradient_device(qf_plan *plan, const double *theta_dev, double *out_
         ck(cudaSetDevice(plan->ctx->device), "cudaSetDevice");
         qf_stats st{};
         enqueue_fused(plan, theta_dev, out_dev, st);
+        st.device_bytes = plan->device_bytes;
         plan->last = st;
     });
 }
@@ -976,3 +977,13 @@ extern "C" int qf_plan_download_psi0(qf_plan *plan, float *psi0_host) {
         ck(cudaStreamSynchronize(plan->ctx->stream), "D2H psi0");
     });
 }
+
+extern "C" int qf_plan_last_stats(const qf_plan *plan, qf_stats *out) {
+    return guarded([&] {
+        if (!plan || !out) throw std::invalid_argument("null argument");
+        *out = plan->last;
+    });
+}
+
+// Error channel for the other translation units of the library (qf_multi.cpp).
+void qfb::set_last_error(const char *msg) { g_err = msg ? msg : ""; }

@@ -200,4 +200,7 @@ cudaError_t launch_reduce_c128(cudaStream_t st, const double *gpart, int gblocks
                                const uint32_t *params, int n_rot, double *grad, const double *epart,
                                uint32_t chunks, uint32_t batch, double *expect, double *loss);
 
+// Sets the thread-local qf_last_error() text (qf_capi.cpp).
+void set_last_error(const char *msg);
+
 } // namespace qfb
