@@ -82,7 +82,7 @@ def test_group_errors():
         with pytest.raises(capi.QfInvalidArgument):
             capi.Group(2, [0, 0])
     with pytest.raises(capi.QfInvalidArgument):
-        capi.gradient_c64_multi(1, gates, 4, npar, 3, 0, psi0, theta, pauli)  # 3 !| periods
+        capi.gradient_c64_multi(1, gates, 4, npar, 2, 3, psi0, theta, pauli)  # k=3 !| 2 layers
     grp = capi.Group(1)
     with pytest.raises(capi.QfInvalidArgument):
         capi.GroupPlan(grp, gates, 4, npar, 2, 0, 0, pauli)  # empty batch
