@@ -127,9 +127,20 @@ def reference_sample(ref, n, layers_total, threads, budget_s=12.0):
         layers *= 2
     sps = batch / dt * (layers / layers_total)
     sample = (f"{n}q x {layers} layers x {batch} samples (run_checkpointed<float>, k=1) in "
-              f"{dt:.2f} s; samples/s extrapolated x{layers}/{layers_total} to the "
-              f"{layers_total}-layer workload")
+              f"{dt:.2f} s on {threads} threads of {cpu_model()} (OpenMP); samples/s "
+              f"extrapolated x{layers}/{layers_total} to the {layers_total}-layer workload")
     return sps, sample, (layers, batch, dt)
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 def host_threads():
