@@ -121,14 +121,25 @@ int qf_gradient_pergate_c64(qf_ctx *ctx, const qf_gate *gates, size_t n_gates,
                             qf_stats *stats_out);
 
 /* complex128 (the reference's double instantiations, engine.cpp:942,
- * checkpoint.cpp:196-213): psi0 is batch*2^(n+1) doubles; per-gate fp64
- * kernels with psi uncomputed in place (ckpt_layers is validated, not needed).
+ * checkpoint.cpp:196-213): psi0 is batch*2^(n+1) doubles. Fused fp64 segments:
+ * each HBM pass applies every op whose target fits one 1024-amplitude tile
+ * (sections of consecutive rotations as one 2x2 unitary, CZ runs, CNOTs),
+ * psi uncomputed in place (ckpt_layers is validated, not needed).
  * Same arguments and errors as qf_gradient_c64. */
 int qf_gradient_c128(qf_ctx *ctx, const qf_gate *gates, size_t n_gates, uint32_t n_qubits,
                      uint32_t n_params, uint32_t layers, uint32_t ckpt_layers,
                      const double *psi0, uint32_t batch, const double *theta,
                      uint64_t x_mask, uint64_t z_mask, double *loss_out, double *grad_out,
                      double *expect_out, qf_stats *stats_out);
+/* complex128 per-gate schedule (one HBM traversal per gate): the reference's
+ * naive_gradient<double> / run_checkpointed_naive<double> (engine.cpp:856-894,
+ * checkpoint.cpp:165-188). Same arguments as qf_gradient_c128. */
+int qf_gradient_pergate_c128(qf_ctx *ctx, const qf_gate *gates, size_t n_gates,
+                             uint32_t n_qubits, uint32_t n_params, uint32_t layers,
+                             uint32_t ckpt_layers, const double *psi0, uint32_t batch,
+                             const double *theta, uint64_t x_mask, uint64_t z_mask,
+                             double *loss_out, double *grad_out, double *expect_out,
+                             qf_stats *stats_out);
 
 /* ---- planned / HBM-resident interface (training loops, bench) ---- */
 

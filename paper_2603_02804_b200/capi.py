@@ -23,6 +23,7 @@ QF_OK, QF_EINVAL, QF_ECAPACITY, QF_EDEVICE = 0, 2, 3, 4
 SYMBOLS = (
     "qf_last_error", "qf_version", "qf_ctx_create", "qf_ctx_destroy", "qf_ctx_set_hbm_limit",
     "qf_gradient_c64", "qf_gradient_c64_ex", "qf_gradient_pergate_c64", "qf_gradient_c128",
+    "qf_gradient_pergate_c128",
     "qf_plan_create",
     "qf_plan_create_ex", "qf_plan_destroy",
     "qf_plan_upload_psi0", "qf_plan_set_psi0_device", "qf_plan_gradient",
@@ -98,6 +99,7 @@ def load(path: str = LIB_PATH):
     L.qf_gradient_pergate_c64.argtypes = grad_args
     L.qf_gradient_c64_ex.argtypes = grad_args[:7] + [C.c_uint32] + grad_args[7:]
     L.qf_gradient_c128.argtypes = grad_args
+    L.qf_gradient_pergate_c128.argtypes = grad_args
     L.qf_plan_create.argtypes = [_P, _P, C.c_size_t, C.c_uint32, C.c_uint32, C.c_uint32,
                                  C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint64, C.POINTER(_P)]
     L.qf_plan_create_ex.argtypes = L.qf_plan_create.argtypes[:-1] + [C.c_uint32, C.POINTER(_P)]
@@ -303,8 +305,9 @@ def gradient_c64(ctx: Context, gates, n_qubits, n_params, layers, ckpt_layers, p
 
 
 def gradient_c128(ctx: Context, gates, n_qubits, n_params, layers, ckpt_layers, psi0, theta,
-                  pauli) -> GradientResult:
-    """qf_gradient_c128: the reference's gradient<double> (complex128 state, fp64 compute)."""
+                  pauli, pergate: bool = False) -> GradientResult:
+    """qf_gradient_c128: the reference's gradient<double> (complex128 state, fp64 compute,
+    fused segments); pergate=True: qf_gradient_pergate_c128 (naive_gradient<double>)."""
     g = _gates(gates)
     a = np.ascontiguousarray(psi0, np.float64)
     batch = a.shape[0]
@@ -313,9 +316,9 @@ def gradient_c128(ctx: Context, gates, n_qubits, n_params, layers, ckpt_layers, 
     exp = np.empty(batch, np.float64)
     loss = C.c_double()
     st = QfStats()
-    _check(_lib.qf_gradient_c128(ctx.h, _ptr(g), len(g), n_qubits, n_params, layers, ckpt_layers,
-                                 _ptr(a), batch, _ptr(th), pauli[0], pauli[1], C.byref(loss),
-                                 _ptr(grad), _ptr(exp), C.byref(st)))
+    fn = _lib.qf_gradient_pergate_c128 if pergate else _lib.qf_gradient_c128
+    _check(fn(ctx.h, _ptr(g), len(g), n_qubits, n_params, layers, ckpt_layers, _ptr(a), batch,
+              _ptr(th), pauli[0], pauli[1], C.byref(loss), _ptr(grad), _ptr(exp), C.byref(st)))
     return GradientResult(loss.value, grad, exp, st.as_dict())
 
 

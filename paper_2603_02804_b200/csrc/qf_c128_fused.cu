@@ -1,0 +1,377 @@
+// complex128 fused path: the reference's double instantiations
+// (gradient<double> engine.cpp:716-755, run_checkpointed<double>
+// checkpoint.cpp:144-163, instantiated at engine.cpp:942 / checkpoint.cpp:196-213)
+// with one HBM pass per *segment* instead of one per gate.
+//
+// Ops (build_c128_plan): a section = a maximal run of consecutive rotations on
+// one qubit, applied as ONE 2x2 unitary U (the rotations multiplied in fp64,
+// later gates on the left, like compose_block_unitary fusion.cpp:127-152); a
+// CZ run = one diagonal sign (apply_cz_kernel engine.cpp:111-136); a CNOT =
+// a conditional pair swap (apply_cnot_kernel engine.cpp:142-170). A segment is
+// a range of ops whose non-diagonal targets fit one tile of 2^m amplitudes in
+// shared memory (m = min(n, 10); qubits 0..2 always local so every 8
+// amplitudes are one 128-B line). One CTA loads a tile (psi, and lambda in
+// the backward), runs the segment's ops on it between __syncthreads, and
+// writes it back.
+//
+// Backward: for each section, in reverse, psi_in = U^dag psi_out and lam_in =
+// U^dag lam_out (psi uncomputed in place: unitary in fp64, the same choice as
+// the per-gate c128 path), and K = sum_pairs psi_in lam_in^dag (2x2) is
+// accumulated. The gradient of rotation j of the section is
+//   Re <lam_out| A_j dg_j B_j |psi_in> = Re Tr(M_j K),  M_j = B_j^dag g_j^dag dg_j B_j
+// (B_j = the rotations before j, A_j after; rotation_derivative
+// circuit.cpp:76-87), evaluated in fp64 by c128_finalize. K partials are
+// reduced per warp (reduce-scatter), per CTA in fixed warp order, and over
+// CTAs in fixed order by the last CTA of the segment: deterministic.
+#include <algorithm>
+#include <set>
+#include <stdexcept>
+
+#include "qf_internal.h"
+
+namespace qfb {
+namespace {
+
+constexpr int kT = 256; // threads per CTA
+
+struct Cx2 { // 2x2 complex, row-major [[a, b], [c, d]]
+    double2 a, b, c, d;
+};
+__device__ __forceinline__ double2 cm(double2 x, double2 y) {
+    return make_double2(x.x * y.x - x.y * y.y, x.x * y.y + x.y * y.x);
+}
+__device__ __forceinline__ double2 cadd(double2 x, double2 y) { return make_double2(x.x + y.x, x.y + y.y); }
+__device__ __forceinline__ double2 cj(double2 x) { return make_double2(x.x, -x.y); }
+__device__ __forceinline__ Cx2 mul(const Cx2 &x, const Cx2 &y) {
+    return {cadd(cm(x.a, y.a), cm(x.b, y.c)), cadd(cm(x.a, y.b), cm(x.b, y.d)),
+            cadd(cm(x.c, y.a), cm(x.d, y.c)), cadd(cm(x.c, y.b), cm(x.d, y.d))};
+}
+__device__ __forceinline__ Cx2 dag(const Cx2 &x) { return {cj(x.a), cj(x.c), cj(x.b), cj(x.d)}; }
+__device__ __forceinline__ Cx2 ident() {
+    return {make_double2(1, 0), make_double2(0, 0), make_double2(0, 0), make_double2(1, 0)};
+}
+// u = c I - i s P (rotation_matrix, circuit.cpp:61-73); with (c, s) ->
+// (-s/2, c/2) the same formula is the derivative (circuit.cpp:76-87).
+__device__ __forceinline__ Cx2 rot(int axis, double c, double s) {
+    const double2 z = make_double2(0, 0);
+    if (axis == 0) return {make_double2(c, 0), make_double2(0, -s), make_double2(0, -s), make_double2(c, 0)};
+    if (axis == 1) return {make_double2(c, 0), make_double2(-s, 0), make_double2(s, 0), make_double2(c, 0)};
+    return {make_double2(c, -s), z, z, make_double2(c, s)};
+}
+
+__global__ void c128_prep(int nsec, const uint32_t *off, const uint32_t *cnt, const uint32_t *gates,
+                          const double *theta, double2 *secU) {
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= nsec) return;
+    Cx2 U = ident();
+    for (uint32_t i = 0; i < cnt[s]; ++i) {
+        const uint32_t g = gates[off[s] + i];
+        double sn, cs;
+        sincos(theta[g >> 2] / 2.0, &sn, &cs);
+        U = mul(rot(int(g & 3u), cs, sn), U);
+    }
+    secU[4 * s + 0] = U.a;
+    secU[4 * s + 1] = U.b;
+    secU[4 * s + 2] = U.c;
+    secU[4 * s + 3] = U.d;
+}
+
+// K layout per section: K00, K01, K10, K11 as (re, im) = 8 doubles.
+__global__ void c128_finalize(int nsec, const uint32_t *off, const uint32_t *cnt,
+                              const uint32_t *gates, const double *theta, const double *K,
+                              double *grad) {
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= nsec) return;
+    const double *k = K + size_t(s) * 8;
+    const Cx2 Kq = {make_double2(k[0], k[1]), make_double2(k[2], k[3]), make_double2(k[4], k[5]),
+                    make_double2(k[6], k[7])};
+    Cx2 B = ident();
+    for (uint32_t i = 0; i < cnt[s]; ++i) {
+        const uint32_t g = gates[off[s] + i];
+        const int axis = int(g & 3u);
+        double sn, cs;
+        sincos(theta[g >> 2] / 2.0, &sn, &cs);
+        const Cx2 u = rot(axis, cs, sn), du = rot(axis, -0.5 * sn, 0.5 * cs);
+        const Cx2 M = mul(dag(B), mul(dag(u), mul(du, B)));
+        const Cx2 MK = mul(M, Kq);
+        grad[g >> 2] = MK.a.x + MK.d.x; // Re Tr(M K)
+        B = mul(u, B);
+    }
+}
+
+__device__ __forceinline__ uint32_t insert0(uint32_t p, uint32_t pos) {
+    return ((p >> pos) << (pos + 1)) | (p & ((1u << pos) - 1u));
+}
+
+template <bool BWD>
+__global__ void __launch_bounds__(kT) seg_c128(const C128Seg sg, const C128Op *__restrict__ ops,
+                                               const uint32_t *__restrict__ czp,
+                                               const double2 *__restrict__ secU, double2 *psi,
+                                               double2 *lam, int n, uint64_t tiles, double *kpart,
+                                               unsigned *ticket, double *K) {
+    extern __shared__ double2 sm[];
+    const uint32_t amps = 1u << sg.m, pairs = amps >> 1;
+    double2 *sp = sm, *sl = sm + amps;
+    double *acc = reinterpret_cast<double *>(sm + (BWD ? 2 * amps : amps)); // [sec][warp][8]
+    const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31u;
+    // the segment's qubit maps, indexed at run time: shared copies (not a local
+    // copy of the parameter block)
+    __shared__ int8_t lpos[32];
+    __shared__ uint8_t lq[16], rq[32];
+    if (tid == 0) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+            lpos[i] = sg.lpos[i];
+            rq[i] = sg.rq[i];
+            if (i < 16) lq[i] = sg.lq[i];
+        }
+    }
+    if (BWD)
+        for (uint32_t i = tid; i < sg.nsec * 64; i += kT) acc[i] = 0.0;
+    __syncthreads();
+    const uint32_t nops = sg.op_end - sg.op_begin;
+    for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const uint64_t base = (t >> sg.nrest) << n;
+        const uint32_t r = uint32_t(t) & ((1u << sg.nrest) - 1u);
+        uint32_t xr = 0;
+        for (uint32_t k = 0; k < sg.nrest; ++k) xr |= ((r >> k) & 1u) << rq[k];
+        uint32_t xs[(1 << kC128TileBits) / kT];
+#pragma unroll
+        for (int k = 0; k < (1 << kC128TileBits) / kT; ++k) {
+            const uint32_t l = tid + uint32_t(k) * kT;
+            if (l < amps) {
+                uint32_t x = xr;
+                for (uint32_t j = 0; j < sg.m; ++j) x |= ((l >> j) & 1u) << lq[j];
+                xs[k] = x;
+                sp[l] = psi[base + x];
+                if (BWD) sl[l] = lam[base + x];
+            }
+        }
+        __syncthreads();
+        for (uint32_t ii = 0; ii < nops; ++ii) {
+            const C128Op op = ops[BWD ? sg.op_end - 1 - ii : sg.op_begin + ii];
+            if (op.type == 0) { // section
+                const uint32_t pos = uint32_t(lpos[op.q]);
+                const double2 *u = secU + 4 * size_t(op.a);
+                const double2 u00 = u[0], u01 = u[1], u10 = u[2], u11 = u[3];
+                if (!BWD) {
+                    for (uint32_t p = tid; p < pairs; p += kT) {
+                        const uint32_t i0 = insert0(p, pos), i1 = i0 | (1u << pos);
+                        const double2 a = sp[i0], b = sp[i1];
+                        sp[i0] = cadd(cm(u00, a), cm(u01, b));
+                        sp[i1] = cadd(cm(u10, a), cm(u11, b));
+                    }
+                } else {
+                    double k8[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+                    // U^dag = [[u00*, u10*], [u01*, u11*]]
+                    const double2 v00 = cj(u00), v01 = cj(u10), v10 = cj(u01), v11 = cj(u11);
+                    for (uint32_t p = tid; p < pairs; p += kT) {
+                        const uint32_t i0 = insert0(p, pos), i1 = i0 | (1u << pos);
+                        const double2 a0 = sp[i0], b0 = sp[i1], la0 = sl[i0], lb0 = sl[i1];
+                        const double2 a = cadd(cm(v00, a0), cm(v01, b0)), b = cadd(cm(v10, a0), cm(v11, b0));
+                        const double2 la = cadd(cm(v00, la0), cm(v01, lb0)),
+                                      lb = cadd(cm(v10, la0), cm(v11, lb0));
+                        sp[i0] = a;
+                        sp[i1] = b;
+                        sl[i0] = la;
+                        sl[i1] = lb;
+                        const double2 k00 = cm(a, cj(la)), k01 = cm(a, cj(lb)), k10 = cm(b, cj(la)),
+                                      k11 = cm(b, cj(lb));
+                        k8[0] += k00.x; k8[1] += k00.y; k8[2] += k01.x; k8[3] += k01.y;
+                        k8[4] += k10.x; k8[5] += k10.y; k8[6] += k11.x; k8[7] += k11.y;
+                    }
+                    // reduce-scatter over 8-lane groups: lane holds value (lane & 7)
+#pragma unroll
+                    for (int m = 4; m >= 1; m >>= 1) {
+                        const bool up = (lane & uint32_t(m)) != 0;
+#pragma unroll
+                        for (int i = 0; i < m; ++i) {
+                            const double send = up ? k8[i] : k8[i + m];
+                            const double keep = up ? k8[i + m] : k8[i];
+                            k8[i] = keep + __shfl_xor_sync(0xffffffffu, send, m);
+                        }
+                    }
+                    double v = k8[0];
+                    v += __shfl_xor_sync(0xffffffffu, v, 8);
+                    v += __shfl_xor_sync(0xffffffffu, v, 16);
+                    if (lane < 8) acc[((op.a - sg.sec_begin) * 8 + warp) * 8 + lane] += v;
+                }
+            } else if (op.type == 1) { // CZ run: one sign per amplitude
+#pragma unroll
+                for (int k = 0; k < (1 << kC128TileBits) / kT; ++k) {
+                    const uint32_t l = tid + uint32_t(k) * kT;
+                    if (l < amps) {
+                        uint32_t f = 0;
+                        for (uint32_t c = 0; c < op.b; ++c) {
+                            const uint32_t w = czp[op.a + c];
+                            f ^= (xs[k] >> (w & 255u)) & (xs[k] >> (w >> 8)) & 1u;
+                        }
+                        if (f) {
+                            sp[l] = make_double2(-sp[l].x, -sp[l].y);
+                            if (BWD) sl[l] = make_double2(-sl[l].x, -sl[l].y);
+                        }
+                    }
+                }
+            } else { // CNOT(control a, target q): self-inverse
+                const uint32_t pos = uint32_t(lpos[op.q]);
+                const int cpos = lpos[op.a];
+                for (uint32_t p = tid; p < pairs; p += kT) {
+                    const uint32_t i0 = insert0(p, pos), i1 = i0 | (1u << pos);
+                    const uint32_t ctl = cpos >= 0 ? (i0 >> cpos) & 1u : (xr >> op.a) & 1u;
+                    if (ctl) {
+                        double2 tmp = sp[i0];
+                        sp[i0] = sp[i1];
+                        sp[i1] = tmp;
+                        if (BWD) {
+                            tmp = sl[i0];
+                            sl[i0] = sl[i1];
+                            sl[i1] = tmp;
+                        }
+                    }
+                }
+            }
+            __syncthreads();
+        }
+#pragma unroll
+        for (int k = 0; k < (1 << kC128TileBits) / kT; ++k) {
+            const uint32_t l = tid + uint32_t(k) * kT;
+            if (l < amps) {
+                psi[base + xs[k]] = sp[l];
+                if (BWD) lam[base + xs[k]] = sl[l];
+            }
+        }
+        __syncthreads();
+    }
+    if (BWD) {
+        const uint32_t nv = sg.nsec * 8;
+        for (uint32_t i = tid; i < nv; i += kT) {
+            const uint32_t s = i >> 3, c = i & 7u;
+            double sum = 0.0;
+            for (int w = 0; w < kT / 32; ++w) sum += acc[(s * 8 + w) * 8 + c];
+            kpart[size_t(blockIdx.x) * nv + i] = sum;
+        }
+        __threadfence();
+        __syncthreads();
+        __shared__ bool last;
+        if (tid == 0) last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+        __syncthreads();
+        if (last) { // fixed-order sum over CTAs
+            __threadfence();
+            for (uint32_t i = tid; i < nv; i += kT) {
+                double sum = 0.0;
+                for (uint32_t b = 0; b < gridDim.x; ++b) sum += __ldcg(kpart + size_t(b) * nv + i);
+                K[size_t(sg.sec_begin) * 8 + i] = sum;
+            }
+            if (tid == 0) *ticket = 0;
+        }
+    }
+}
+
+} // namespace
+
+C128Plan build_c128_plan(const qf_gate *gates, size_t n_gates, uint32_t n) {
+    C128Plan P;
+    for (size_t i = 0; i < n_gates; ++i) {
+        const qf_gate &g = gates[i];
+        if (g.kind == QF_GATE_ROTATION) {
+            if (!P.ops.empty() && P.ops.back().type == 0 && P.ops.back().q == g.q0) {
+                P.sec_cnt.back()++;
+            } else {
+                P.ops.push_back({0u, g.q0, uint32_t(P.sec_off.size()), 0u});
+                P.sec_off.push_back(uint32_t(P.sec_gates.size()));
+                P.sec_cnt.push_back(1u);
+            }
+            P.sec_gates.push_back(uint32_t(g.axis) | (g.param << 2));
+        } else if (g.kind == QF_GATE_CZ) {
+            if (P.ops.empty() || P.ops.back().type != 1)
+                P.ops.push_back({1u, 0u, uint32_t(P.cz.size()), 0u});
+            P.cz.push_back(g.q0 | (g.q1 << 8));
+            P.ops.back().b++;
+        } else {
+            P.ops.push_back({2u, g.q1, g.q0, 0u});
+        }
+    }
+    const uint32_t m = std::min<uint32_t>(n, kC128TileBits);
+    const uint32_t nbase = std::min<uint32_t>(n, 3);
+    size_t i = 0;
+    uint32_t sec = 0;
+    while (i < P.ops.size() || (P.ops.empty() && P.segs.empty())) {
+        std::set<uint32_t> S;
+        for (uint32_t q = 0; q < nbase; ++q) S.insert(q);
+        uint32_t nsec = 0;
+        size_t j = i;
+        for (; j < P.ops.size(); ++j) {
+            const C128Op &op = P.ops[j];
+            const bool needs = op.type != 1;
+            if (needs && !S.count(op.q) && S.size() + 1 > m) break;
+            if (op.type == 0 && nsec == uint32_t(kC128MaxSec)) break;
+            if (needs) S.insert(op.q);
+            if (op.type == 0) ++nsec;
+        }
+        for (uint32_t q = 0; S.size() < m; ++q) S.insert(q);
+        C128Seg sg{};
+        sg.m = m;
+        sg.nrest = n - m;
+        sg.op_begin = uint32_t(i);
+        sg.op_end = uint32_t(j);
+        sg.sec_begin = sec;
+        sg.nsec = nsec;
+        for (int q = 0; q < 32; ++q) sg.lpos[q] = -1;
+        uint32_t l = 0, r = 0;
+        for (uint32_t q = 0; q < n; ++q) {
+            if (S.count(q)) {
+                sg.lq[l] = uint8_t(q);
+                sg.lpos[q] = int8_t(l++);
+            } else {
+                sg.rq[r++] = uint8_t(q);
+            }
+        }
+        P.segs.push_back(sg);
+        sec += nsec;
+        if (j == i) break; // empty circuit: one segment that only copies
+        i = j;
+    }
+    return P;
+}
+
+int c128_seg_grid(int sms, uint64_t tiles) {
+    const uint64_t cap = uint64_t(sms) * 4;
+    return int(std::max<uint64_t>(1, std::min(tiles, cap)));
+}
+
+cudaError_t launch_c128_prep(cudaStream_t st, int nsec, const uint32_t *off, const uint32_t *cnt,
+                             const uint32_t *gates, const double *theta, double2 *secU) {
+    if (nsec == 0) return cudaSuccess;
+    c128_prep<<<(nsec + 127) / 128, 128, 0, st>>>(nsec, off, cnt, gates, theta, secU);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_c128_segment(cudaStream_t st, bool backward, int grid, const C128Seg &sg,
+                                const C128Op *ops, const uint32_t *cz, const double2 *secU,
+                                double2 *psi, double2 *lam, int n, uint32_t batch, double *kpart,
+                                unsigned *ticket, double *K) {
+    const uint64_t tiles = uint64_t(batch) << sg.nrest;
+    const size_t amps = size_t(1) << sg.m;
+    if (backward) {
+        const size_t smem = amps * 2 * sizeof(double2) + size_t(kC128MaxSec) * 64 * sizeof(double);
+        static const cudaError_t attr = cudaFuncSetAttribute(
+            seg_c128<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            int((size_t(2) << kC128TileBits) * sizeof(double2) + size_t(kC128MaxSec) * 64 * sizeof(double)));
+        if (attr != cudaSuccess) return attr;
+        seg_c128<true><<<grid, kT, smem, st>>>(sg, ops, cz, secU, psi, lam, n, tiles, kpart, ticket, K);
+    } else {
+        const size_t smem = amps * sizeof(double2);
+        seg_c128<false><<<grid, kT, smem, st>>>(sg, ops, cz, secU, psi, lam, n, tiles, kpart, ticket, K);
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_c128_finalize(cudaStream_t st, int nsec, const uint32_t *off, const uint32_t *cnt,
+                                 const uint32_t *gates, const double *theta, const double *K,
+                                 double *grad) {
+    if (nsec == 0) return cudaSuccess;
+    c128_finalize<<<(nsec + 127) / 128, 128, 0, st>>>(nsec, off, cnt, gates, theta, K, grad);
+    return cudaGetLastError();
+}
+
+} // namespace qfb

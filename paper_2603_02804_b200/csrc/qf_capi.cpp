@@ -641,6 +641,140 @@ void run_host(qf_plan *pl, const double *theta, double *loss, double *grad, doub
     if (stats) *stats = st;
 }
 
+// complex128 driver. fused: one HBM pass per segment (qf_c128_fused.cu);
+// otherwise one per gate (qf_c128.cu, the reference's naive_gradient<double>).
+// psi is uncomputed in place in fp64 either way (no checkpoint slots needed;
+// ckpt_layers is validated like the complex64 path).
+void run_c128(qf_ctx *ctx, const qf_gate *gates, size_t n_gates, uint32_t n_qubits,
+              uint32_t n_params, uint32_t layers, uint32_t ckpt_layers, const double *psi0,
+              uint32_t batch, const double *theta, uint64_t x_mask, uint64_t z_mask,
+              double *loss_out, double *grad_out, double *expect_out, qf_stats *stats_out,
+              bool fused) {
+    if (!ctx) throw std::invalid_argument("null context");
+    if (!psi0) throw std::invalid_argument("null psi0");
+    // same validation (and error messages) as the complex64 path
+    const Plan P = make_plan(gates, n_gates, n_qubits, n_params, layers, ckpt_layers, batch, x_mask, z_mask);
+    if (P.n_params && !theta) throw std::invalid_argument("gradient: theta length mismatch");
+    if (!loss_out || (P.n_params && !grad_out)) throw std::invalid_argument("gradient: null output");
+    ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+    cudaStream_t s = ctx->stream;
+    const uint32_t n = P.n;
+    const uint64_t amps = uint64_t(batch) << n;
+    const size_t state_bytes = size_t(amps) * sizeof(double2);
+    const uint64_t dim = 1ull << n;
+    const uint32_t chunks = dim >= 4096 ? uint32_t(dim / 4096) : 1u;
+    std::vector<uint32_t> rp;
+    for (const qf_gate &g : P.gates)
+        if (g.kind == QF_GATE_ROTATION) rp.push_back(g.param);
+    const int n_rot = int(rp.size());
+    const C128Plan F = fused ? build_c128_plan(P.gates.data(), P.gates.size(), n) : C128Plan{};
+    const int nsec = int(F.sec_off.size());
+    const int seg_grid = fused ? c128_seg_grid(ctx->sms, uint64_t(batch) << (n - F.segs[0].m)) : 0;
+    const int gblocks = fused ? 0 : c128_gate_grid(std::max<uint64_t>(1, amps / 2));
+    const size_t scratch = fused ? (size_t(nsec) * 8 + size_t(seg_grid) * kC128MaxSec * 8 +
+                                    size_t(nsec) * 8) * 8
+                                 : size_t(std::max(1, n_rot)) * gblocks * 8;
+    size_t free_b = 0, total_b = 0;
+    ck(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
+    const uint64_t budget = ctx->hbm_limit ? std::min<uint64_t>(ctx->hbm_limit, free_b) : free_b;
+    const size_t need = 2 * state_bytes + scratch + (size_t(64) << 20);
+    if (need > budget)
+        throw CapacityError("device working set of " + std::to_string(need >> 20) +
+                            " MiB exceeds the HBM budget of " + std::to_string(budget >> 20) + " MiB");
+    std::vector<void *> owned;
+    struct Free {
+        std::vector<void *> &v;
+        ~Free() {
+            for (void *p : v) cudaFree(p);
+        }
+    } guard{owned};
+    double2 *psi = dalloc<double2>(amps, owned), *lam = dalloc<double2>(amps, owned);
+    double *th = dalloc<double>(std::max<uint32_t>(1, P.n_params), owned);
+    double *epart = dalloc<double>(size_t(batch) * chunks, owned);
+    double *out = dalloc<double>(size_t(P.n_params) + 1 + batch, owned);
+    ck(cudaMemcpyAsync(psi, psi0, state_bytes, cudaMemcpyHostToDevice, s), "H2D psi0");
+    if (P.n_params)
+        ck(cudaMemcpyAsync(th, theta, sizeof(double) * P.n_params, cudaMemcpyHostToDevice, s), "H2D theta");
+    ck(cudaMemsetAsync(out, 0, sizeof(double) * (size_t(P.n_params) + 1 + batch), s), "memset");
+    double *grad_d = out, *loss_d = out + P.n_params, *exp_d = out + P.n_params + 1;
+    qf_stats st{};
+    struct Events {
+        cudaEvent_t a = nullptr, b = nullptr;
+        ~Events() {
+            if (a) cudaEventDestroy(a);
+            if (b) cudaEventDestroy(b);
+        }
+    } ev;
+    ck(cudaEventCreate(&ev.a), "event");
+    ck(cudaEventCreate(&ev.b), "event");
+    ck(cudaEventRecord(ev.a, s), "event"); // device time: kernels only (psi0 already resident)
+    if (fused) {
+        C128Op *ops = dupload(F.ops, owned);
+        uint32_t *cz = dupload(F.cz, owned);
+        uint32_t *soff = dupload(F.sec_off, owned), *scnt = dupload(F.sec_cnt, owned),
+                 *sgat = dupload(F.sec_gates, owned);
+        double2 *secU = dalloc<double2>(size_t(std::max(1, nsec)) * 4, owned);
+        double *K = dalloc<double>(size_t(std::max(1, nsec)) * 8, owned);
+        double *kpart = dalloc<double>(size_t(seg_grid) * kC128MaxSec * 8, owned);
+        unsigned *ticket = dalloc<unsigned>(1, owned);
+        ck(cudaMemsetAsync(ticket, 0, sizeof(unsigned), s), "memset");
+        ck(launch_c128_prep(s, nsec, soff, scnt, sgat, th, secU), "c128 prep");
+        for (const C128Seg &sg : F.segs) {
+            ck(launch_c128_segment(s, false, seg_grid, sg, ops, cz, secU, psi, lam, int(n), batch,
+                                   kpart, ticket, K),
+               "c128 segment");
+            st.forward_passes++;
+        }
+        ck(launch_seed_c128(s, int(n), batch, P.x_mask, P.z_mask, P.y_count, psi, lam, chunks, epart),
+           "c128 seed");
+        for (size_t i = F.segs.size(); i-- > 0;) {
+            ck(launch_c128_segment(s, true, seg_grid, F.segs[i], ops, cz, secU, psi, lam, int(n),
+                                   batch, kpart, ticket, K),
+               "c128 segment");
+            st.backward_passes++;
+        }
+        ck(launch_c128_finalize(s, nsec, soff, scnt, sgat, th, K, grad_d), "c128 finalize");
+        ck(launch_reduce_c128(s, nullptr, 0, nullptr, 0, grad_d, epart, chunks, batch, exp_d, loss_d),
+           "c128 reduce");
+        st.kernel_launches = st.forward_passes + st.backward_passes + 4;
+    } else {
+        double *gpart = dalloc<double>(size_t(std::max(1, n_rot)) * gblocks, owned);
+        uint32_t *params = dupload(rp, owned);
+        for (const qf_gate &g : P.gates) {
+            ck(launch_gate_fwd_c128(s, psi, int(n), batch, g.kind, g.axis, g.q0, g.q1, th, g.param), "c128 fwd");
+            st.forward_passes++;
+        }
+        ck(launch_seed_c128(s, int(n), batch, P.x_mask, P.z_mask, P.y_count, psi, lam, chunks, epart), "c128 seed");
+        int r = n_rot;
+        for (size_t i = P.gates.size(); i-- > 0;) {
+            const qf_gate &g = P.gates[i];
+            double *gp = g.kind == QF_GATE_ROTATION ? gpart + size_t(--r) * gblocks : nullptr;
+            ck(launch_gate_bwd_c128(s, psi, lam, int(n), batch, g.kind, g.axis, g.q0, g.q1, th, g.param, gp),
+               "c128 bwd");
+            st.backward_passes++;
+        }
+        ck(launch_reduce_c128(s, gpart, gblocks, params, n_rot, grad_d, epart, chunks, batch, exp_d, loss_d),
+           "c128 reduce");
+        st.kernel_launches = st.forward_passes + st.backward_passes + 2;
+    }
+    ck(cudaEventRecord(ev.b, s), "event");
+    std::vector<double> h(size_t(P.n_params) + 1 + batch);
+    ck(cudaMemcpyAsync(h.data(), out, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, s), "D2H");
+    ck(cudaStreamSynchronize(s), "c128 gradient");
+    float dev_ms = 0.f;
+    ck(cudaEventElapsedTime(&dev_ms, ev.a, ev.b), "elapsed");
+    st.device_ms = dev_ms;
+    *loss_out = h[P.n_params];
+    if (P.n_params) std::memcpy(grad_out, h.data(), sizeof(double) * P.n_params);
+    if (expect_out) std::memcpy(expect_out, h.data() + P.n_params + 1, sizeof(double) * batch);
+    st.observable_passes = 1;
+    st.hbm_bytes = uint64_t((2.0 * st.forward_passes + 4.0 * st.backward_passes + 2.0) * state_bytes);
+    st.device_bytes = 2 * state_bytes;
+    st.passes_per_layer = P.layers ? uint32_t((st.forward_passes + P.layers - 1) / P.layers) : 0;
+    st.stages = P.stages;
+    if (stats_out) *stats_out = st;
+}
+
 } // namespace
 
 extern "C" {
@@ -842,78 +976,19 @@ int qf_gradient_c128(qf_ctx *ctx, const qf_gate *gates, size_t n_gates, uint32_t
                      uint32_t batch, const double *theta, uint64_t x_mask, uint64_t z_mask,
                      double *loss_out, double *grad_out, double *expect_out, qf_stats *stats_out) {
     return guarded([&] {
-        if (!ctx) throw std::invalid_argument("null context");
-        if (!psi0) throw std::invalid_argument("null psi0");
-        // same validation (and error messages) as the complex64 path
-        const Plan P = make_plan(gates, n_gates, n_qubits, n_params, layers, ckpt_layers, batch, x_mask, z_mask);
-        if (P.n_params && !theta) throw std::invalid_argument("gradient: theta length mismatch");
-        if (!loss_out || (P.n_params && !grad_out)) throw std::invalid_argument("gradient: null output");
-        ck(cudaSetDevice(ctx->device), "cudaSetDevice");
-        cudaStream_t s = ctx->stream;
-        const uint32_t n = P.n;
-        const uint64_t amps = uint64_t(batch) << n;
-        const size_t state_bytes = size_t(amps) * sizeof(double2);
-        const uint64_t dim = 1ull << n;
-        const uint32_t chunks = dim >= 4096 ? uint32_t(dim / 4096) : 1u;
-        std::vector<uint32_t> rp;
-        for (const qf_gate &g : P.gates)
-            if (g.kind == QF_GATE_ROTATION) rp.push_back(g.param);
-        const int n_rot = int(rp.size());
-        const int gblocks = c128_gate_grid(std::max<uint64_t>(1, amps / 2));
-        size_t free_b = 0, total_b = 0;
-        ck(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
-        const uint64_t budget = ctx->hbm_limit ? std::min<uint64_t>(ctx->hbm_limit, free_b) : free_b;
-        const size_t need = 2 * state_bytes + size_t(std::max(1, n_rot)) * gblocks * 8 + (size_t(64) << 20);
-        if (need > budget)
-            throw CapacityError("device working set of " + std::to_string(need >> 20) +
-                                " MiB exceeds the HBM budget of " + std::to_string(budget >> 20) + " MiB");
-        std::vector<void *> owned;
-        struct Free {
-            std::vector<void *> &v;
-            ~Free() {
-                for (void *p : v) cudaFree(p);
-            }
-        } guard{owned};
-        double2 *psi = dalloc<double2>(amps, owned), *lam = dalloc<double2>(amps, owned);
-        double *th = dalloc<double>(std::max<uint32_t>(1, P.n_params), owned);
-        double *gpart = dalloc<double>(size_t(std::max(1, n_rot)) * gblocks, owned);
-        double *epart = dalloc<double>(size_t(batch) * chunks, owned);
-        double *out = dalloc<double>(size_t(P.n_params) + 1 + batch, owned);
-        uint32_t *params = dupload(rp, owned);
-        ck(cudaMemcpyAsync(psi, psi0, state_bytes, cudaMemcpyHostToDevice, s), "H2D psi0");
-        if (P.n_params)
-            ck(cudaMemcpyAsync(th, theta, sizeof(double) * P.n_params, cudaMemcpyHostToDevice, s), "H2D theta");
-        ck(cudaMemsetAsync(out, 0, sizeof(double) * (size_t(P.n_params) + 1 + batch), s), "memset");
-        qf_stats st{};
-        for (const qf_gate &g : P.gates) {
-            ck(launch_gate_fwd_c128(s, psi, int(n), batch, g.kind, g.axis, g.q0, g.q1, th, g.param), "c128 fwd");
-            st.forward_passes++;
-        }
-        ck(launch_seed_c128(s, int(n), batch, P.x_mask, P.z_mask, P.y_count, psi, lam, chunks, epart), "c128 seed");
-        st.observable_passes = 1;
-        int r = n_rot;
-        for (size_t i = P.gates.size(); i-- > 0;) {
-            const qf_gate &g = P.gates[i];
-            double *gp = g.kind == QF_GATE_ROTATION ? gpart + size_t(--r) * gblocks : nullptr;
-            ck(launch_gate_bwd_c128(s, psi, lam, int(n), batch, g.kind, g.axis, g.q0, g.q1, th, g.param, gp),
-               "c128 bwd");
-            st.backward_passes++;
-        }
-        double *grad_d = out, *loss_d = out + P.n_params, *exp_d = out + P.n_params + 1;
-        ck(launch_reduce_c128(s, gpart, gblocks, params, n_rot, grad_d, epart, chunks, batch, exp_d, loss_d),
-           "c128 reduce");
-        std::vector<double> h(size_t(P.n_params) + 1 + batch);
-        ck(cudaMemcpyAsync(h.data(), out, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, s), "D2H");
-        ck(cudaStreamSynchronize(s), "c128 gradient");
-        *loss_out = h[P.n_params];
-        if (P.n_params) std::memcpy(grad_out, h.data(), sizeof(double) * P.n_params);
-        if (expect_out) std::memcpy(expect_out, h.data() + P.n_params + 1, sizeof(double) * batch);
-        st.kernel_launches = st.forward_passes + st.backward_passes + 2;
-        st.hbm_bytes = uint64_t((2.0 * st.forward_passes + 4.0 * st.backward_passes + 2.0) * state_bytes);
-        st.device_bytes = 2 * state_bytes;
-        st.passes_per_layer = P.layers ? uint32_t(P.gates.size() / P.layers) : 0;
-        st.stages = P.stages;
-        if (stats_out) *stats_out = st;
+        run_c128(ctx, gates, n_gates, n_qubits, n_params, layers, ckpt_layers, psi0, batch, theta,
+                 x_mask, z_mask, loss_out, grad_out, expect_out, stats_out, /*fused=*/true);
+    });
+}
+
+int qf_gradient_pergate_c128(qf_ctx *ctx, const qf_gate *gates, size_t n_gates, uint32_t n_qubits,
+                             uint32_t n_params, uint32_t layers, uint32_t ckpt_layers,
+                             const double *psi0, uint32_t batch, const double *theta,
+                             uint64_t x_mask, uint64_t z_mask, double *loss_out, double *grad_out,
+                             double *expect_out, qf_stats *stats_out) {
+    return guarded([&] {
+        run_c128(ctx, gates, n_gates, n_qubits, n_params, layers, ckpt_layers, psi0, batch, theta,
+                 x_mask, z_mask, loss_out, grad_out, expect_out, stats_out, /*fused=*/false);
     });
 }
 

@@ -5,9 +5,12 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <vector>
 
 #include <cuda.h>
 #include <cuda_runtime.h>
+
+#include "../../include/qfuse_b200.h"
 
 namespace qfb {
 
@@ -199,6 +202,45 @@ cudaError_t launch_seed_c128(cudaStream_t st, int n, uint32_t batch, uint64_t x_
 cudaError_t launch_reduce_c128(cudaStream_t st, const double *gpart, int gblocks,
                                const uint32_t *params, int n_rot, double *grad, const double *epart,
                                uint32_t chunks, uint32_t batch, double *expect, double *loss);
+
+// complex128 fused path (qf_c128_fused.cu). The circuit becomes a list of ops —
+// a *section* (maximal run of consecutive rotations on one qubit, one 2x2
+// unitary), a CZ run (one diagonal), a CNOT — cut into *segments*: op ranges
+// whose non-diagonal targets fit one shared-memory tile of 2^m amplitudes
+// (m = min(n, 10), local qubits 0..2 always included for coalescing). A segment
+// is one HBM pass; the backward measures K = sum psi_in lam_in^dag per section
+// and the gradients of the section's rotations are Re Tr(M_j K) (c128_finalize).
+constexpr int kC128TileBits = 10;
+constexpr int kC128MaxSec = 32; // sections per segment (shared K accumulators)
+struct C128Op {
+    uint32_t type; // 0 section, 1 CZ run, 2 CNOT
+    uint32_t q;    // section qubit / CNOT target
+    uint32_t a;    // section index / first CZ pair / CNOT control
+    uint32_t b;    // CZ pair count
+};
+struct C128Seg {
+    uint32_t m, nrest, op_begin, op_end, sec_begin, nsec;
+    int8_t lpos[32]; // qubit -> local bit, -1 if the qubit indexes tiles
+    uint8_t lq[16];  // local bit -> qubit (ascending)
+    uint8_t rq[32];  // tile bit -> qubit (ascending)
+};
+struct C128Plan {
+    std::vector<C128Op> ops;
+    std::vector<C128Seg> segs;
+    std::vector<uint32_t> cz;        // q0 | q1 << 8
+    std::vector<uint32_t> sec_off, sec_cnt, sec_gates; // gates: axis | param << 2
+};
+C128Plan build_c128_plan(const qf_gate *gates, size_t n_gates, uint32_t n);
+int c128_seg_grid(int sms, uint64_t tiles);
+cudaError_t launch_c128_prep(cudaStream_t st, int nsec, const uint32_t *off, const uint32_t *cnt,
+                             const uint32_t *gates, const double *theta, double2 *secU);
+cudaError_t launch_c128_segment(cudaStream_t st, bool backward, int grid, const C128Seg &sg,
+                                const C128Op *ops, const uint32_t *cz, const double2 *secU,
+                                double2 *psi, double2 *lam, int n, uint32_t batch, double *kpart,
+                                unsigned *ticket, double *K);
+cudaError_t launch_c128_finalize(cudaStream_t st, int nsec, const uint32_t *off, const uint32_t *cnt,
+                                 const uint32_t *gates, const double *theta, const double *K,
+                                 double *grad);
 
 // Sets the thread-local qf_last_error() text (qf_capi.cpp).
 void set_last_error(const char *msg);

@@ -102,13 +102,15 @@ GradientResult call(bool pergate, const std::vector<Gate> &flat, uint32_t n_qubi
     return r;
 }
 
-// complex128: every call runs the fp64 per-gate device path; MemSave has no
-// effect there (no slots are stored), as in the reference at double where
-// the narrowed type is float (statevec.hpp narrow_traits<double>).
-GradientResult call_c128(const std::vector<Gate> &flat, uint32_t n_qubits, uint32_t n_params,
-                         uint32_t layers, uint32_t block_layers, const BatchedState<double> &psi0,
-                         std::span<const double> theta, const PauliString &pauli,
-                         MemoryAccountant *accountant) {
+// complex128: gradient/run_checkpointed run the fused fp64 segments
+// (qf_gradient_c128), naive_gradient/run_checkpointed_naive the fp64 per-gate
+// path (qf_gradient_pergate_c128). MemSave has no effect there (no slots are
+// stored), as in the reference at double where the narrowed type is float
+// (statevec.hpp narrow_traits<double>).
+GradientResult call_c128(bool naive, const std::vector<Gate> &flat, uint32_t n_qubits,
+                         uint32_t n_params, uint32_t layers, uint32_t block_layers,
+                         const BatchedState<double> &psi0, std::span<const double> theta,
+                         const PauliString &pauli, MemoryAccountant *accountant) {
     if (psi0.n_qubits() != pauli.n_qubits)
         throw std::invalid_argument("engine: state qubit count mismatch"); // engine.cpp:438-442
     if (theta.size() != n_params)
@@ -117,9 +119,10 @@ GradientResult call_c128(const std::vector<Gate> &flat, uint32_t n_qubits, uint3
     GradientResult r;
     r.gradient.assign(n_params, 0.0);
     qf_stats st{};
-    check(qf_gradient_c128(context(), gates.data(), gates.size(), n_qubits, n_params, layers,
-                           block_layers, psi0.components().data(), psi0.batch(), theta.data(),
-                           pauli.x_mask, pauli.z_mask, &r.loss, r.gradient.data(), nullptr, &st));
+    check((naive ? qf_gradient_pergate_c128 : qf_gradient_c128)(
+        context(), gates.data(), gates.size(), n_qubits, n_params, layers, block_layers,
+        psi0.components().data(), psi0.batch(), theta.data(), pauli.x_mask, pauli.z_mask, &r.loss,
+        r.gradient.data(), nullptr, &st));
     r.stats.forward_traversals = st.forward_passes;
     r.stats.backward_traversals = st.backward_passes;
     r.stats.observable_traversals = st.observable_passes;
@@ -138,7 +141,7 @@ void set_device(int device) { t_device = device; }
 GradientResult gradient(const FusedCircuit &fused, const BatchedState<double> &psi0,
                         std::span<const double> theta, const PauliString &pauli,
                         StorageMode, MemoryAccountant *accountant) {
-    return call_c128(flatten(fused), fused.n_qubits, fused.n_params, 0, 0, psi0, theta, pauli, accountant);
+    return call_c128(false, flatten(fused), fused.n_qubits, fused.n_params, 0, 0, psi0, theta, pauli, accountant);
 }
 
 GradientResult run_checkpointed(const FusedCircuit &fused, const BatchedState<double> &psi0,
@@ -146,14 +149,14 @@ GradientResult run_checkpointed(const FusedCircuit &fused, const BatchedState<do
                                 const CheckpointPlan &plan, StorageMode, MemoryAccountant *accountant) {
     if (plan.ops_per_layer * plan.layers != fused.ops.size()) // checkpoint.cpp:149-151
         throw std::invalid_argument("run_checkpointed: plan does not cover the circuit");
-    return call_c128(flatten(fused), fused.n_qubits, fused.n_params, plan.layers, plan.block_layers,
+    return call_c128(false, flatten(fused), fused.n_qubits, fused.n_params, plan.layers, plan.block_layers,
                      psi0, theta, pauli, accountant);
 }
 
 GradientResult naive_gradient(const Circuit &circuit, const BatchedState<double> &psi0,
                               std::span<const double> theta, const PauliString &pauli,
                               MemoryAccountant *accountant) {
-    return call_c128(circuit.gates(), circuit.n_qubits(), circuit.n_params(), 0, 0, psi0, theta,
+    return call_c128(true, circuit.gates(), circuit.n_qubits(), circuit.n_params(), 0, 0, psi0, theta,
                      pauli, accountant);
 }
 
@@ -190,7 +193,7 @@ GradientResult run_checkpointed_naive(const Circuit &circuit, const BatchedState
                                       const CheckpointPlan &plan, MemoryAccountant *accountant) {
     if (plan.ops_per_layer * plan.layers != circuit.gates().size())
         throw std::invalid_argument("run_checkpointed_naive: plan does not cover the circuit");
-    return call_c128(circuit.gates(), circuit.n_qubits(), circuit.n_params(), plan.layers,
+    return call_c128(true, circuit.gates(), circuit.n_qubits(), circuit.n_params(), plan.layers,
                      plan.block_layers, psi0, theta, pauli, accountant);
 }
 

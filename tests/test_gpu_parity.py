@@ -413,6 +413,49 @@ def test_c128_hea(ctx, oracle, n, layers, batch):
     _check64(res, oracle.gradient(gates, n, npar, psi0, theta, pauli))
 
 
+@pytest.mark.parametrize("n,ngates,seed", [(3, 30, 5), (11, 120, 6), (14, 160, 7), (17, 90, 8)])
+def test_c128_fused_vs_pergate(ctx, n, ngates, seed):
+    """Fused fp64 segments == the fp64 per-gate schedule (acceptance C2, fused
+    == per-gate at 1e-12, acceptance.cpp:137-170), random Rx/Ry/Rz/CZ/CNOT
+    circuits with several segments (n > 10) and CNOT controls off-tile."""
+    gates, npar = C.random_circuit(n, ngates, seed)
+    theta = C.random_parameters(npar, seed + 100)
+    psi0 = C.new_random_state(n, 2, seed + 200, np.float64)
+    pauli = C.parse_pauli(C.repeated_ixyz_label(n))
+    fused = capi.gradient_c128(ctx, gates, n, npar, 0, 0, psi0, theta, pauli)
+    naive = capi.gradient_c128(ctx, gates, n, npar, 0, 0, psi0, theta, pauli, pergate=True)
+    assert np.max(np.abs(fused.gradient - naive.gradient)) <= 1e-12
+    assert abs(fused.loss - naive.loss) <= 1e-12
+    np.testing.assert_allclose(fused.expect, naive.expect, rtol=0, atol=1e-12)
+    assert fused.stats["forward_passes"] < naive.stats["forward_passes"]
+
+
+def test_c128_fused_segments_hea(ctx, oracle):
+    """16q HEA: 2-3 segments per layer instead of 4n gate passes; vs the oracle."""
+    n, layers, batch = 16, 3, 2
+    gates, npar = C.build_hea(n, layers)
+    theta = C.random_parameters(npar, 31)
+    psi0 = C.new_random_state(n, batch, 32, np.float64)
+    pauli = C.parse_pauli(C.repeated_ixyz_label(n))
+    res = capi.gradient_c128(ctx, gates, n, npar, layers, 0, psi0, theta, pauli)
+    _check64(res, oracle.gradient(gates, n, npar, psi0, theta, pauli))
+    assert res.stats["forward_passes"] <= 3 * layers
+    again = capi.gradient_c128(ctx, gates, n, npar, layers, 0, psi0, theta, pauli)
+    np.testing.assert_array_equal(again.gradient, res.gradient)  # deterministic reductions
+
+
+def test_c128_no_rotations(ctx, oracle):
+    gates = np.zeros(2, dtype=C.GATE_DTYPE)
+    gates[0] = (C.CZ, 0, 0, 0, 1, 0)
+    gates[1] = (C.CNOT, 0, 0, 2, 0, 0)
+    psi0 = C.new_random_state(3, 2, 5, np.float64)
+    pauli = C.parse_pauli("XYZ")
+    res = capi.gradient_c128(ctx, gates, 3, 0, 0, 0, psi0, np.zeros(0), pauli)
+    loss, _, exp = oracle.gradient(gates, 3, 0, psi0, np.zeros(0), pauli)
+    assert abs(res.loss - loss) <= 1e-12
+    np.testing.assert_allclose(res.expect, exp, atol=1e-12)
+
+
 def test_c128_against_reference_double(ctx, ref):
     """The unmodified reference's gradient<double> on the same inputs."""
     n, layers, batch = 8, 6, 4
