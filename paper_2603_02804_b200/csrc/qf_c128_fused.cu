@@ -99,12 +99,18 @@ __global__ void c128_finalize(int nsec, const uint32_t *off, const uint32_t *cnt
     }
 }
 
+// Shared-memory slot of tile amplitude l: the low 3 bits are XORed with 7 when
+// bit 3 is set, so the 8 lanes of a quarter-warp hit 8 distinct 16-B bank groups
+// for pair accesses on every local bit (bits 0..2 would otherwise be 2-way
+// conflicted) and for consecutive amplitudes.
+__device__ __forceinline__ uint32_t sw(uint32_t l) { return l ^ (((l >> 3) & 1u) * 7u); }
+
 __device__ __forceinline__ uint32_t insert0(uint32_t p, uint32_t pos) {
     return ((p >> pos) << (pos + 1)) | (p & ((1u << pos) - 1u));
 }
 
 template <bool BWD>
-__global__ void __launch_bounds__(kT) seg_c128(const C128Seg sg, const C128Op *__restrict__ ops,
+__global__ void __launch_bounds__(kT, 2) seg_c128(const C128Seg sg, const C128Op *__restrict__ ops,
                                                const uint32_t *__restrict__ czp,
                                                const double2 *__restrict__ secU, double2 *psi,
                                                double2 *lam, int n, uint64_t tiles, double *kpart,
@@ -130,22 +136,53 @@ __global__ void __launch_bounds__(kT) seg_c128(const C128Seg sg, const C128Op *_
         for (uint32_t i = tid; i < sg.nsec * 64; i += kT) acc[i] = 0.0;
     __syncthreads();
     const uint32_t nops = sg.op_end - sg.op_begin;
-    for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
-        const uint64_t base = (t >> sg.nrest) << n;
+    constexpr int KA = (1 << kC128TileBits) / kT; // amplitudes per thread
+    // local part of the global index of this thread's amplitudes (fixed per segment)
+    uint32_t xl[KA];
+#pragma unroll
+    for (int k = 0; k < KA; ++k) {
+        const uint32_t l = tid + uint32_t(k) * kT;
+        uint32_t x = 0;
+        for (uint32_t j = 0; j < sg.m; ++j) x |= ((l >> j) & 1u) << lq[j];
+        xl[k] = x;
+    }
+    auto tile_xr = [&](uint64_t t) {
         const uint32_t r = uint32_t(t) & ((1u << sg.nrest) - 1u);
         uint32_t xr = 0;
         for (uint32_t k = 0; k < sg.nrest; ++k) xr |= ((r >> k) & 1u) << rq[k];
-        uint32_t xs[(1 << kC128TileBits) / kT];
+        return xr;
+    };
+    // the next tile is loaded into registers while the current one is processed
+    double2 ra[KA], rl[KA];
+    auto fetch = [&](uint64_t t, uint32_t xr) {
+        const uint64_t base = (t >> sg.nrest) << n;
 #pragma unroll
-        for (int k = 0; k < (1 << kC128TileBits) / kT; ++k) {
-            const uint32_t l = tid + uint32_t(k) * kT;
-            if (l < amps) {
-                uint32_t x = xr;
-                for (uint32_t j = 0; j < sg.m; ++j) x |= ((l >> j) & 1u) << lq[j];
-                xs[k] = x;
-                sp[l] = psi[base + x];
-                if (BWD) sl[l] = lam[base + x];
+        for (int k = 0; k < KA; ++k)
+            if (tid + uint32_t(k) * kT < amps) {
+                ra[k] = psi[base + (xr | xl[k])];
+                if (BWD) rl[k] = lam[base + (xr | xl[k])];
             }
+    };
+    uint64_t t = blockIdx.x;
+    uint32_t xr = t < tiles ? tile_xr(t) : 0u;
+    if (t < tiles) fetch(t, xr);
+    for (; t < tiles; t += gridDim.x) {
+        const uint64_t base = (t >> sg.nrest) << n;
+        uint32_t xs[KA];
+#pragma unroll
+        for (int k = 0; k < KA; ++k) {
+            const uint32_t l = tid + uint32_t(k) * kT;
+            xs[k] = xr | xl[k];
+            if (l < amps) {
+                sp[sw(l)] = ra[k];
+                if (BWD) sl[sw(l)] = rl[k];
+            }
+        }
+        const uint32_t xr_cur = xr;
+        const uint64_t tn = t + gridDim.x;
+        if (tn < tiles) {
+            xr = tile_xr(tn);
+            fetch(tn, xr);
         }
         __syncthreads();
         for (uint32_t ii = 0; ii < nops; ++ii) {
@@ -157,9 +194,9 @@ __global__ void __launch_bounds__(kT) seg_c128(const C128Seg sg, const C128Op *_
                 if (!BWD) {
                     for (uint32_t p = tid; p < pairs; p += kT) {
                         const uint32_t i0 = insert0(p, pos), i1 = i0 | (1u << pos);
-                        const double2 a = sp[i0], b = sp[i1];
-                        sp[i0] = cadd(cm(u00, a), cm(u01, b));
-                        sp[i1] = cadd(cm(u10, a), cm(u11, b));
+                        const double2 a = sp[sw(i0)], b = sp[sw(i1)];
+                        sp[sw(i0)] = cadd(cm(u00, a), cm(u01, b));
+                        sp[sw(i1)] = cadd(cm(u10, a), cm(u11, b));
                     }
                 } else {
                     double k8[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -167,14 +204,14 @@ __global__ void __launch_bounds__(kT) seg_c128(const C128Seg sg, const C128Op *_
                     const double2 v00 = cj(u00), v01 = cj(u10), v10 = cj(u01), v11 = cj(u11);
                     for (uint32_t p = tid; p < pairs; p += kT) {
                         const uint32_t i0 = insert0(p, pos), i1 = i0 | (1u << pos);
-                        const double2 a0 = sp[i0], b0 = sp[i1], la0 = sl[i0], lb0 = sl[i1];
+                        const double2 a0 = sp[sw(i0)], b0 = sp[sw(i1)], la0 = sl[sw(i0)], lb0 = sl[sw(i1)];
                         const double2 a = cadd(cm(v00, a0), cm(v01, b0)), b = cadd(cm(v10, a0), cm(v11, b0));
                         const double2 la = cadd(cm(v00, la0), cm(v01, lb0)),
                                       lb = cadd(cm(v10, la0), cm(v11, lb0));
-                        sp[i0] = a;
-                        sp[i1] = b;
-                        sl[i0] = la;
-                        sl[i1] = lb;
+                        sp[sw(i0)] = a;
+                        sp[sw(i1)] = b;
+                        sl[sw(i0)] = la;
+                        sl[sw(i1)] = lb;
                         const double2 k00 = cm(a, cj(la)), k01 = cm(a, cj(lb)), k10 = cm(b, cj(la)),
                                       k11 = cm(b, cj(lb));
                         k8[0] += k00.x; k8[1] += k00.y; k8[2] += k01.x; k8[3] += k01.y;
@@ -198,7 +235,7 @@ __global__ void __launch_bounds__(kT) seg_c128(const C128Seg sg, const C128Op *_
                 }
             } else if (op.type == 1) { // CZ run: one sign per amplitude
 #pragma unroll
-                for (int k = 0; k < (1 << kC128TileBits) / kT; ++k) {
+                for (int k = 0; k < KA; ++k) {
                     const uint32_t l = tid + uint32_t(k) * kT;
                     if (l < amps) {
                         uint32_t f = 0;
@@ -207,8 +244,8 @@ __global__ void __launch_bounds__(kT) seg_c128(const C128Seg sg, const C128Op *_
                             f ^= (xs[k] >> (w & 255u)) & (xs[k] >> (w >> 8)) & 1u;
                         }
                         if (f) {
-                            sp[l] = make_double2(-sp[l].x, -sp[l].y);
-                            if (BWD) sl[l] = make_double2(-sl[l].x, -sl[l].y);
+                            sp[sw(l)] = make_double2(-sp[sw(l)].x, -sp[sw(l)].y);
+                            if (BWD) sl[sw(l)] = make_double2(-sl[sw(l)].x, -sl[sw(l)].y);
                         }
                     }
                 }
@@ -217,15 +254,15 @@ __global__ void __launch_bounds__(kT) seg_c128(const C128Seg sg, const C128Op *_
                 const int cpos = lpos[op.a];
                 for (uint32_t p = tid; p < pairs; p += kT) {
                     const uint32_t i0 = insert0(p, pos), i1 = i0 | (1u << pos);
-                    const uint32_t ctl = cpos >= 0 ? (i0 >> cpos) & 1u : (xr >> op.a) & 1u;
+                    const uint32_t ctl = cpos >= 0 ? (i0 >> cpos) & 1u : (xr_cur >> op.a) & 1u;
                     if (ctl) {
-                        double2 tmp = sp[i0];
-                        sp[i0] = sp[i1];
-                        sp[i1] = tmp;
+                        double2 tmp = sp[sw(i0)];
+                        sp[sw(i0)] = sp[sw(i1)];
+                        sp[sw(i1)] = tmp;
                         if (BWD) {
-                            tmp = sl[i0];
-                            sl[i0] = sl[i1];
-                            sl[i1] = tmp;
+                            tmp = sl[sw(i0)];
+                            sl[sw(i0)] = sl[sw(i1)];
+                            sl[sw(i1)] = tmp;
                         }
                     }
                 }
@@ -233,11 +270,11 @@ __global__ void __launch_bounds__(kT) seg_c128(const C128Seg sg, const C128Op *_
             __syncthreads();
         }
 #pragma unroll
-        for (int k = 0; k < (1 << kC128TileBits) / kT; ++k) {
+        for (int k = 0; k < KA; ++k) {
             const uint32_t l = tid + uint32_t(k) * kT;
             if (l < amps) {
-                psi[base + xs[k]] = sp[l];
-                if (BWD) lam[base + xs[k]] = sl[l];
+                psi[base + xs[k]] = sp[sw(l)];
+                if (BWD) lam[base + xs[k]] = sl[sw(l)];
             }
         }
         __syncthreads();
@@ -335,7 +372,7 @@ C128Plan build_c128_plan(const qf_gate *gates, size_t n_gates, uint32_t n) {
 }
 
 int c128_seg_grid(int sms, uint64_t tiles) {
-    const uint64_t cap = uint64_t(sms) * 4;
+    const uint64_t cap = uint64_t(sms) * 2; // 2 CTAs/SM (registers: the next tile is prefetched)
     return int(std::max<uint64_t>(1, std::min(tiles, cap)));
 }
 
