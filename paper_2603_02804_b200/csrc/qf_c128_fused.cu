@@ -109,6 +109,51 @@ __device__ __forceinline__ uint32_t insert0(uint32_t p, uint32_t pos) {
     return ((p >> pos) << (pos + 1)) | (p & ((1u << pos) - 1u));
 }
 
+__device__ __forceinline__ void cp_async16(void *smem_dst, const void *gmem_src) {
+    const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(smem_dst));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(gmem_src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+struct U2 { // a section's unitary, or its adjoint
+    double2 u00, u01, u10, u11;
+};
+__device__ __forceinline__ U2 load_u(const double2 *secU, uint32_t s, bool adjoint) {
+    const double2 *u = secU + 4 * size_t(s);
+    const double2 a = u[0], b = u[1], c = u[2], d = u[3];
+    return adjoint ? U2{cj(a), cj(c), cj(b), cj(d)} : U2{a, b, c, d};
+}
+__device__ __forceinline__ void apply_u(const U2 &u, double2 &a, double2 &b) {
+    const double2 a0 = a, b0 = b;
+    a = cadd(cm(u.u00, a0), cm(u.u01, b0));
+    b = cadd(cm(u.u10, a0), cm(u.u11, b0));
+}
+// K += [a; b] [la; lb]^dag (8 doubles: K00, K01, K10, K11 as re, im)
+__device__ __forceinline__ void kacc(double (&k8)[8], double2 a, double2 b, double2 la, double2 lb) {
+    const double2 k00 = cm(a, cj(la)), k01 = cm(a, cj(lb)), k10 = cm(b, cj(la)), k11 = cm(b, cj(lb));
+    k8[0] += k00.x; k8[1] += k00.y; k8[2] += k01.x; k8[3] += k01.y;
+    k8[4] += k10.x; k8[5] += k10.y; k8[6] += k11.x; k8[7] += k11.y;
+}
+// Warp sum of the 8 values (reduce-scatter over 8-lane groups, then across the
+// groups), added by lanes 0..7 to this warp's accumulator slot.
+__device__ __forceinline__ void kflush(double (&k8)[8], uint32_t lane, double *slot) {
+#pragma unroll
+    for (int m = 4; m >= 1; m >>= 1) {
+        const bool up = (lane & uint32_t(m)) != 0;
+#pragma unroll
+        for (int i = 0; i < m; ++i) {
+            const double send = up ? k8[i] : k8[i + m];
+            const double keep = up ? k8[i + m] : k8[i];
+            k8[i] = keep + __shfl_xor_sync(0xffffffffu, send, m);
+        }
+    }
+    double v = k8[0];
+    v += __shfl_xor_sync(0xffffffffu, v, 8);
+    v += __shfl_xor_sync(0xffffffffu, v, 16);
+    if (lane < 8) slot[lane] += v;
+}
+
 template <bool BWD>
 __global__ void __launch_bounds__(kT, 2) seg_c128(const C128Seg sg, const C128Op *__restrict__ ops,
                                                const uint32_t *__restrict__ czp,
@@ -117,8 +162,9 @@ __global__ void __launch_bounds__(kT, 2) seg_c128(const C128Seg sg, const C128Op
                                                unsigned *ticket, double *K) {
     extern __shared__ double2 sm[];
     const uint32_t amps = 1u << sg.m, pairs = amps >> 1;
-    double2 *sp = sm, *sl = sm + amps;
-    double *acc = reinterpret_cast<double *>(sm + (BWD ? 2 * amps : amps)); // [sec][warp][8]
+    constexpr uint32_t kBufs = BWD ? 2u : 1u; // psi (+ lambda) per tile buffer
+    // two tile buffers: tile i+1 is copied in (cp.async) while tile i is processed
+    double *acc = reinterpret_cast<double *>(sm + 2 * kBufs * amps); // [sec][warp][8]
     const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31u;
     // the segment's qubit maps, indexed at run time: shared copies (not a local
     // copy of the parameter block)
@@ -152,87 +198,110 @@ __global__ void __launch_bounds__(kT, 2) seg_c128(const C128Seg sg, const C128Op
         for (uint32_t k = 0; k < sg.nrest; ++k) xr |= ((r >> k) & 1u) << rq[k];
         return xr;
     };
-    // the next tile is loaded into registers while the current one is processed
-    double2 ra[KA], rl[KA];
-    auto fetch = [&](uint64_t t, uint32_t xr) {
+    auto fetch = [&](uint64_t t, uint32_t buf) {
         const uint64_t base = (t >> sg.nrest) << n;
-#pragma unroll
-        for (int k = 0; k < KA; ++k)
-            if (tid + uint32_t(k) * kT < amps) {
-                ra[k] = psi[base + (xr | xl[k])];
-                if (BWD) rl[k] = lam[base + (xr | xl[k])];
-            }
-    };
-    uint64_t t = blockIdx.x;
-    uint32_t xr = t < tiles ? tile_xr(t) : 0u;
-    if (t < tiles) fetch(t, xr);
-    for (; t < tiles; t += gridDim.x) {
-        const uint64_t base = (t >> sg.nrest) << n;
-        uint32_t xs[KA];
+        const uint32_t xr = tile_xr(t);
+        double2 *dp = sm + buf * kBufs * amps;
 #pragma unroll
         for (int k = 0; k < KA; ++k) {
             const uint32_t l = tid + uint32_t(k) * kT;
-            xs[k] = xr | xl[k];
             if (l < amps) {
-                sp[sw(l)] = ra[k];
-                if (BWD) sl[sw(l)] = rl[k];
+                cp_async16(dp + sw(l), psi + base + (xr | xl[k]));
+                if (BWD) cp_async16(dp + amps + sw(l), lam + base + (xr | xl[k]));
             }
         }
-        const uint32_t xr_cur = xr;
-        const uint64_t tn = t + gridDim.x;
-        if (tn < tiles) {
-            xr = tile_xr(tn);
-            fetch(tn, xr);
-        }
+        cp_async_commit();
+    };
+    uint32_t it = 0;
+    if (blockIdx.x < tiles) fetch(blockIdx.x, 0);
+    for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
+        const uint32_t buf = it & 1u;
+        double2 *sp = sm + buf * kBufs * amps, *sl = sp + amps;
+        const uint64_t base = (t >> sg.nrest) << n;
+        const uint32_t xr_cur = tile_xr(t);
+        uint32_t xs[KA];
+#pragma unroll
+        for (int k = 0; k < KA; ++k) xs[k] = xr_cur | xl[k];
+        cp_async_wait_all();
         __syncthreads();
+        if (t + gridDim.x < tiles) fetch(t + gridDim.x, buf ^ 1u);
         for (uint32_t ii = 0; ii < nops; ++ii) {
             const C128Op op = ops[BWD ? sg.op_end - 1 - ii : sg.op_begin + ii];
-            if (op.type == 0) { // section
-                const uint32_t pos = uint32_t(lpos[op.q]);
-                const double2 *u = secU + 4 * size_t(op.a);
-                const double2 u00 = u[0], u01 = u[1], u10 = u[2], u11 = u[3];
-                if (!BWD) {
-                    for (uint32_t p = tid; p < pairs; p += kT) {
-                        const uint32_t i0 = insert0(p, pos), i1 = i0 | (1u << pos);
-                        const double2 a = sp[sw(i0)], b = sp[sw(i1)];
-                        sp[sw(i0)] = cadd(cm(u00, a), cm(u01, b));
-                        sp[sw(i1)] = cadd(cm(u10, a), cm(u11, b));
-                    }
-                } else {
-                    double k8[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-                    // U^dag = [[u00*, u10*], [u01*, u11*]]
-                    const double2 v00 = cj(u00), v01 = cj(u10), v10 = cj(u01), v11 = cj(u11);
-                    for (uint32_t p = tid; p < pairs; p += kT) {
-                        const uint32_t i0 = insert0(p, pos), i1 = i0 | (1u << pos);
-                        const double2 a0 = sp[sw(i0)], b0 = sp[sw(i1)], la0 = sl[sw(i0)], lb0 = sl[sw(i1)];
-                        const double2 a = cadd(cm(v00, a0), cm(v01, b0)), b = cadd(cm(v10, a0), cm(v11, b0));
-                        const double2 la = cadd(cm(v00, la0), cm(v01, lb0)),
-                                      lb = cadd(cm(v10, la0), cm(v11, lb0));
-                        sp[sw(i0)] = a;
-                        sp[sw(i1)] = b;
-                        sl[sw(i0)] = la;
-                        sl[sw(i1)] = lb;
-                        const double2 k00 = cm(a, cj(la)), k01 = cm(a, cj(lb)), k10 = cm(b, cj(la)),
-                                      k11 = cm(b, cj(lb));
-                        k8[0] += k00.x; k8[1] += k00.y; k8[2] += k01.x; k8[3] += k01.y;
-                        k8[4] += k10.x; k8[5] += k10.y; k8[6] += k11.x; k8[7] += k11.y;
-                    }
-                    // reduce-scatter over 8-lane groups: lane holds value (lane & 7)
+            if (op.type == 0 && ii + 1 < nops && amps >= 4) {
+                const C128Op op2 = ops[BWD ? sg.op_end - 2 - ii : sg.op_begin + ii + 1];
+                if (op2.type == 0 && op2.q != op.q) {
+                    // two sections on different qubits in one round: each thread
+                    // owns a quad (bits p1, p2) and applies (or undoes) op then op2
+                    // in registers; K of both is measured after both are undone
+                    // (K of a qubit is invariant under gates on other qubits)
+                    const uint32_t p1 = uint32_t(lpos[op.q]), p2 = uint32_t(lpos[op2.q]);
+                    const uint32_t lo = min(p1, p2), hi = max(p1, p2);
+                    const U2 ua = load_u(secU, op.a, BWD), ub = load_u(secU, op2.a, BWD);
+                    double ka[8] = {0, 0, 0, 0, 0, 0, 0, 0}, kb[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+                    if (tid < (amps >> 2)) { // amps / 4 <= kT: one quad per thread
+                        const uint32_t b0 = insert0(insert0(tid, lo), hi);
+                        uint32_t ix[2][2];
+                        double2 v[2][2], w[2][2];
 #pragma unroll
-                    for (int m = 4; m >= 1; m >>= 1) {
-                        const bool up = (lane & uint32_t(m)) != 0;
+                        for (int i = 0; i < 2; ++i)
 #pragma unroll
-                        for (int i = 0; i < m; ++i) {
-                            const double send = up ? k8[i] : k8[i + m];
-                            const double keep = up ? k8[i + m] : k8[i];
-                            k8[i] = keep + __shfl_xor_sync(0xffffffffu, send, m);
+                            for (int j = 0; j < 2; ++j) {
+                                ix[i][j] = sw(b0 | (uint32_t(i) << p1) | (uint32_t(j) << p2));
+                                v[i][j] = sp[ix[i][j]];
+                                if (BWD) w[i][j] = sl[ix[i][j]];
+                            }
+#pragma unroll
+                        for (int j = 0; j < 2; ++j) {
+                            apply_u(ua, v[0][j], v[1][j]);
+                            if (BWD) apply_u(ua, w[0][j], w[1][j]);
                         }
+#pragma unroll
+                        for (int i = 0; i < 2; ++i) {
+                            apply_u(ub, v[i][0], v[i][1]);
+                            if (BWD) apply_u(ub, w[i][0], w[i][1]);
+                        }
+                        if (BWD) {
+#pragma unroll
+                            for (int j = 0; j < 2; ++j) kacc(ka, v[0][j], v[1][j], w[0][j], w[1][j]);
+#pragma unroll
+                            for (int i = 0; i < 2; ++i) kacc(kb, v[i][0], v[i][1], w[i][0], w[i][1]);
+                        }
+#pragma unroll
+                        for (int i = 0; i < 2; ++i)
+#pragma unroll
+                            for (int j = 0; j < 2; ++j) {
+                                sp[ix[i][j]] = v[i][j];
+                                if (BWD) sl[ix[i][j]] = w[i][j];
+                            }
                     }
-                    double v = k8[0];
-                    v += __shfl_xor_sync(0xffffffffu, v, 8);
-                    v += __shfl_xor_sync(0xffffffffu, v, 16);
-                    if (lane < 8) acc[((op.a - sg.sec_begin) * 8 + warp) * 8 + lane] += v;
+                    if (BWD) {
+                        kflush(ka, lane, acc + ((op.a - sg.sec_begin) * 8 + warp) * 8);
+                        kflush(kb, lane, acc + ((op2.a - sg.sec_begin) * 8 + warp) * 8);
+                    }
+                    ++ii;
+                    __syncthreads();
+                    continue;
                 }
+            }
+            if (op.type == 0) { // a single section
+                const uint32_t pos = uint32_t(lpos[op.q]);
+                const U2 u = load_u(secU, op.a, BWD);
+                double k8[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+                for (uint32_t p = tid; p < pairs; p += kT) {
+                    const uint32_t i0 = sw(insert0(p, pos)), i1 = sw(insert0(p, pos) | (1u << pos));
+                    double2 a = sp[i0], b = sp[i1];
+                    apply_u(u, a, b);
+                    sp[i0] = a;
+                    sp[i1] = b;
+                    if (BWD) {
+                        double2 la = sl[i0], lb = sl[i1];
+                        apply_u(u, la, lb);
+                        sl[i0] = la;
+                        sl[i1] = lb;
+                        kacc(k8, a, b, la, lb);
+                    }
+                }
+                if (BWD) kflush(k8, lane, acc + ((op.a - sg.sec_begin) * 8 + warp) * 8);
             } else if (op.type == 1) { // CZ run: one sign per amplitude
 #pragma unroll
                 for (int k = 0; k < KA; ++k) {
@@ -372,7 +441,7 @@ C128Plan build_c128_plan(const qf_gate *gates, size_t n_gates, uint32_t n) {
 }
 
 int c128_seg_grid(int sms, uint64_t tiles) {
-    const uint64_t cap = uint64_t(sms) * 2; // 2 CTAs/SM (registers: the next tile is prefetched)
+    const uint64_t cap = uint64_t(sms) * 2; // 2 CTAs/SM (backward: 80 KiB smem, <= 128 registers)
     return int(std::max<uint64_t>(1, std::min(tiles, cap)));
 }
 
@@ -390,14 +459,14 @@ cudaError_t launch_c128_segment(cudaStream_t st, bool backward, int grid, const 
     const uint64_t tiles = uint64_t(batch) << sg.nrest;
     const size_t amps = size_t(1) << sg.m;
     if (backward) {
-        const size_t smem = amps * 2 * sizeof(double2) + size_t(kC128MaxSec) * 64 * sizeof(double);
+        const size_t smem = amps * 4 * sizeof(double2) + size_t(kC128MaxSec) * 64 * sizeof(double);
         static const cudaError_t attr = cudaFuncSetAttribute(
             seg_c128<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-            int((size_t(2) << kC128TileBits) * sizeof(double2) + size_t(kC128MaxSec) * 64 * sizeof(double)));
+            int((size_t(4) << kC128TileBits) * sizeof(double2) + size_t(kC128MaxSec) * 64 * sizeof(double)));
         if (attr != cudaSuccess) return attr;
         seg_c128<true><<<grid, kT, smem, st>>>(sg, ops, cz, secU, psi, lam, n, tiles, kpart, ticket, K);
     } else {
-        const size_t smem = amps * sizeof(double2);
+        const size_t smem = amps * 2 * sizeof(double2);
         seg_c128<false><<<grid, kT, smem, st>>>(sg, ops, cz, secU, psi, lam, n, tiles, kpart, ticket, K);
     }
     return cudaGetLastError();
