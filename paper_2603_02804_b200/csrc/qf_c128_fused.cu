@@ -192,6 +192,23 @@ __global__ void __launch_bounds__(kT, 2) seg_c128(const C128Seg sg, const C128Op
         for (uint32_t j = 0; j < sg.m; ++j) x |= ((l >> j) & 1u) << lq[j];
         xl[k] = x;
     }
+    // Q(xl) of every CZ run of the segment (op.q = its index < kC128MaxCz)
+    uint32_t qlb[KA];
+#pragma unroll
+    for (int k = 0; k < KA; ++k) qlb[k] = 0;
+    for (uint32_t i = sg.op_begin; i < sg.op_end; ++i) {
+        const C128Op op = ops[i];
+        if (op.type != 1) continue;
+#pragma unroll
+        for (int k = 0; k < KA; ++k) {
+            uint32_t f = 0;
+            for (uint32_t c = 0; c < op.b; ++c) {
+                const uint32_t w = czp[op.a + c];
+                f ^= (xl[k] >> (w & 255u)) & (xl[k] >> (w >> 8)) & 1u;
+            }
+            qlb[k] |= f << op.q;
+        }
+    }
     auto tile_xr = [&](uint64_t t) {
         const uint32_t r = uint32_t(t) & ((1u << sg.nrest) - 1u);
         uint32_t xr = 0;
@@ -303,19 +320,23 @@ __global__ void __launch_bounds__(kT, 2) seg_c128(const C128Seg sg, const C128Op
                 }
                 if (BWD) kflush(k8, lane, acc + ((op.a - sg.sec_begin) * 8 + warp) * 8);
             } else if (op.type == 1) { // CZ run: one sign per amplitude
+                // Q(xr | xl) = Q(xr) ^ Q(xl) ^ parity(xl & M(xr)), M(xr) = the qubits
+                // with an odd number of CZ partners set in xr: the per-pair loop runs
+                // once per tile (warp-uniform) instead of once per amplitude, and
+                // Q(xl) of this thread's amplitudes is precomputed (qlb, bit op.q).
+                uint32_t qr = 0, M = 0;
+                for (uint32_t c = 0; c < op.b; ++c) {
+                    const uint32_t w = czp[op.a + c], a = w & 255u, b = w >> 8;
+                    const uint32_t ra = (xr_cur >> a) & 1u, rb = (xr_cur >> b) & 1u;
+                    qr ^= ra & rb;
+                    M ^= (ra << b) ^ (rb << a);
+                }
 #pragma unroll
                 for (int k = 0; k < KA; ++k) {
                     const uint32_t l = tid + uint32_t(k) * kT;
-                    if (l < amps) {
-                        uint32_t f = 0;
-                        for (uint32_t c = 0; c < op.b; ++c) {
-                            const uint32_t w = czp[op.a + c];
-                            f ^= (xs[k] >> (w & 255u)) & (xs[k] >> (w >> 8)) & 1u;
-                        }
-                        if (f) {
-                            sp[sw(l)] = make_double2(-sp[sw(l)].x, -sp[sw(l)].y);
-                            if (BWD) sl[sw(l)] = make_double2(-sl[sw(l)].x, -sl[sw(l)].y);
-                        }
+                    if (l < amps && (qr ^ ((qlb[k] >> op.q) & 1u) ^ (__popc(xl[k] & M) & 1u))) {
+                        sp[sw(l)] = make_double2(-sp[sw(l)].x, -sp[sw(l)].y);
+                        if (BWD) sl[sw(l)] = make_double2(-sl[sw(l)].x, -sl[sw(l)].y);
                     }
                 }
             } else { // CNOT(control a, target q): self-inverse
@@ -404,15 +425,17 @@ C128Plan build_c128_plan(const qf_gate *gates, size_t n_gates, uint32_t n) {
     while (i < P.ops.size() || (P.ops.empty() && P.segs.empty())) {
         std::set<uint32_t> S;
         for (uint32_t q = 0; q < nbase; ++q) S.insert(q);
-        uint32_t nsec = 0;
+        uint32_t nsec = 0, ncz = 0;
         size_t j = i;
         for (; j < P.ops.size(); ++j) {
             const C128Op &op = P.ops[j];
             const bool needs = op.type != 1;
             if (needs && !S.count(op.q) && S.size() + 1 > m) break;
             if (op.type == 0 && nsec == uint32_t(kC128MaxSec)) break;
+            if (op.type == 1 && ncz == uint32_t(kC128MaxCz)) break;
             if (needs) S.insert(op.q);
             if (op.type == 0) ++nsec;
+            if (op.type == 1) P.ops[j].q = ncz++; // index of the CZ run within its segment
         }
         for (uint32_t q = 0; S.size() < m; ++q) S.insert(q);
         C128Seg sg{};

@@ -212,9 +212,10 @@ cudaError_t launch_reduce_c128(cudaStream_t st, const double *gpart, int gblocks
 // and the gradients of the section's rotations are Re Tr(M_j K) (c128_finalize).
 constexpr int kC128TileBits = 10;
 constexpr int kC128MaxSec = 32; // sections per segment (shared K accumulators)
+constexpr int kC128MaxCz = 32;  // CZ runs per segment (one bit each in a register mask)
 struct C128Op {
     uint32_t type; // 0 section, 1 CZ run, 2 CNOT
-    uint32_t q;    // section qubit / CNOT target
+    uint32_t q;    // section qubit / CNOT target / CZ run index within its segment
     uint32_t a;    // section index / first CZ pair / CNOT control
     uint32_t b;    // CZ pair count
 };
