@@ -116,10 +116,8 @@ struct qf_group {
     std::mutex mu; // calls on one group are serialised
 
     ~qf_group() {
-        if (!comms.empty()) {
-            const Nccl &api = nccl();
-            for (ncclComm_t c : comms) api.comm_destroy(c);
-        }
+        for (ncclComm_t c : comms)
+            if (c) nccl().comm_destroy(c); // non-null only once NCCL was loaded
         for (qf_ctx *c : ctx) qf_ctx_destroy(c);
     }
 };
@@ -177,8 +175,9 @@ qf_group *make_group(int n_gpus, const int *devices) {
         g->ctx.push_back(c);
     }
     const Nccl &api = nccl();
-    g->comms.resize(n_gpus);
-    api.check(api.comm_init_all(g->comms.data(), n_gpus, devs.data()), "ncclCommInitAll");
+    std::vector<ncclComm_t> comms(n_gpus, nullptr);
+    api.check(api.comm_init_all(comms.data(), n_gpus, devs.data()), "ncclCommInitAll");
+    g->comms = comms;
     return g.release();
 }
 
@@ -250,11 +249,13 @@ void group_gradient(qf_group_plan *gp, const double *theta, double *loss, double
     }
     // 2) the single exchange: [grad | loss] summed over the group, in place
     api.check(api.group_start(), "ncclGroupStart");
-    for (int i = 0; i < G; ++i)
-        api.check(api.all_reduce(gp->dev[i].out, gp->dev[i].out, R, ncclFloat64, ncclSum,
-                                 g->comms[i], gp->dev[i].stream),
-                  "ncclAllReduce");
-    api.check(api.group_end(), "ncclGroupEnd");
+    ncclResult_t rr = ncclSuccess;
+    for (int i = 0; i < G && rr == ncclSuccess; ++i)
+        rr = api.all_reduce(gp->dev[i].out, gp->dev[i].out, R, ncclFloat64, ncclSum, g->comms[i],
+                            gp->dev[i].stream);
+    const ncclResult_t re = api.group_end(); // always close the group
+    api.check(rr, "ncclAllReduce");
+    api.check(re, "ncclGroupEnd");
     // 3) results: the reduced vector from device 0, each shard's expectations
     for (int i = 0; i < G; ++i) {
         qf_group_plan::Dev &d = gp->dev[i];
