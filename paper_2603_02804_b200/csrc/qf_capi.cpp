@@ -9,6 +9,7 @@
 // into a ledger, checkpoint.cpp:123-135; both give the same gradients).
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cstdlib>
@@ -103,6 +104,17 @@ CUtensorMap flat_map(void *base, uint64_t rows, uint64_t nbuf, uint64_t buf_byte
     cuuint32_t box[3] = {32, 256, 1};
     return encode(base, 3, dims, strides, box);
 }
+
+// NVTX range around the host enqueue of one phase of a gradient (forward passes,
+// observable, backward passes, reductions): `ncu --nvtx --nvtx-include
+// "qfuse backward/"` selects one phase's kernels. Header-only NVTX: a no-op
+// unless a tool is attached.
+struct Nvtx {
+    explicit Nvtx(const char *name) { nvtxRangePushA(name); }
+    ~Nvtx() { nvtxRangePop(); }
+    Nvtx(const Nvtx &) = delete;
+    Nvtx &operator=(const Nvtx &) = delete;
+};
 
 template <class T> T *dalloc(size_t count, std::vector<void *> &owned) {
     if (count == 0) count = 1;
@@ -449,6 +461,7 @@ void enqueue_fused(qf_plan *pl, const double *theta_dev, double *out_dev, qf_sta
                                           : pl->slots + size_t(P.n_slots - 1) * pl->amps_padded;
         auto slot16 = [&](size_t pi) { return pl->slots16 + size_t(pi / P.ckpt_passes) * pl->amps_padded; };
         // forward (MemSave: every pass in place on W; a slot pass is narrowed into its bf16 slot)
+        std::unique_ptr<Nvtx> range(new Nvtx("qfuse forward"));
         for (size_t pi = 0; pi < NPS; ++pi) {
             const PassStep &ps = P.steps[pi];
             const CUtensorMap *in;
@@ -482,10 +495,14 @@ void enqueue_fused(qf_plan *pl, const double *theta_dev, double *out_dev, qf_sta
         sp.lam = pl->lam;
         sp.epart = pl->epart;
         sp.apply_only = forward_only ? 1 : 0;
+        range.reset(); // pop before the next push (NVTX ranges are a stack)
+        range.reset(new Nvtx("qfuse observable"));
         pl->timed(2, 2 * sb, [&] { ck(launch_seed(s, sp), "seed"); });
         st.kernel_launches++;
         st.observable_passes++;
         bytes += 2 * sb;
+        range.reset();
+        range.reset(new Nvtx("qfuse backward"));
         if (!forward_only) {
             for (size_t pi = NPS; pi-- > 0;) {
                 const PassStep &ps = P.steps[pi];
@@ -509,6 +526,7 @@ void enqueue_fused(qf_plan *pl, const double *theta_dev, double *out_dev, qf_sta
                 bytes += (write_psi ? 4 : 3) * sb;
             }
         }
+        range.reset();
         st.passes_per_layer = S ? uint32_t((NPS + S - 1) / S) : 0;
         st.resident = 0;
     }
