@@ -91,16 +91,29 @@ class ClockSampler:
                 if len(parts) >= 9:
                     rows.append(parts)
         os.unlink(self.tmp.name)
-        if not rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        if not rows:  # timed region shorter than nvidia-smi's start-up: one query right after
+            try:
+                out = subprocess.run(["nvidia-smi", f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits", "-i", str(self.gpu)],
+                                     capture_output=True, text=True, timeout=20).stdout
+                rows = [[x.strip() for x in line.split(",")] for line in out.splitlines()
+                        if len(line.split(",")) >= 9]
+            except (OSError, subprocess.TimeoutExpired):
+                rows = []
+            if not rows:
+                return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+            self.note = "sampled once right after the timed region (region shorter than the sampler start-up)"
         sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
         mx = max(float(r[2]) for r in rows if r[2].replace(".", "").isdigit())
         loaded = [s for s in sm if s > 0.5 * mx] or sm
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i] == "Active"})
         power = [float(r[3]) for r in rows if r[3].replace(".", "").isdigit()]
-        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": mx, "reasons": reasons,
-                "samples": len(rows), "power_w_max": max(power) if power else None}
+        res = {"sm_mhz": statistics.median(loaded), "sm_max_mhz": mx, "reasons": reasons,
+               "samples": len(rows), "power_w_max": max(power) if power else None}
+        if getattr(self, "note", None):
+            res["note"] = self.note
+        return res
 
 
 # ------------------------------------------------------------ CPU legs
