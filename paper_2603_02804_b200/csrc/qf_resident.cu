@@ -268,6 +268,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         // ---------------- forward over all stages
         for (int s = 0; s < S; ++s) {
             const PhaseEnv e = env_for(s);
+            if (s + 1 < S) load_stage(s + 1); // other slot: its latency overlaps this stage
             run_phase_fwd(0, pt, tid, 2u | 4u, e);
             __syncthreads();
             if (rot & 0xF0u) {
@@ -275,7 +276,6 @@ __global__ void __launch_bounds__(kThreads, 2)
                 __syncthreads();
             }
             if (rot & 0xF00u) run_phase_fwd(2, pt, tid, 4u, e);
-            if (s + 1 < S) load_stage(s + 1);
             const bool slot = ((s + 1) % p.ckpt == 0) && (s + 1 < S) && !p.forward_only;
             if (slot) fence_async_smem();
             __syncthreads();
@@ -342,6 +342,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                 phase ^= 1u;
             }
             const PhaseEnv e = env_for(s);
+            if (s > 0) load_stage(s - 1); // other slot: its latency overlaps this stage
             if (rot & 0xF00u) {
                 run_phase_bwd(2, pt, lt, tid, 4u, e);
                 __syncthreads();
@@ -351,7 +352,6 @@ __global__ void __launch_bounds__(kThreads, 2)
                 __syncthreads();
             }
             run_phase_bwd(0, pt, lt, tid, 4u | 2u, e);
-            if (s > 0) load_stage(s - 1);
             __syncthreads();
             if (tid < 96) {
                 const int lb = tid >> 3, c = tid & 7;
@@ -363,7 +363,10 @@ __global__ void __launch_bounds__(kThreads, 2)
                         sum += *a;
                         *a = 0.0;
                     }
-                    p.kpart[(size_t(blockIdx.x) * S + s) * size_t(n) * 8 + lb * 8 + c] += sum;
+                    // fire-and-forget RED (no load round trip before the barrier); the
+                    // slot is private to this CTA and this thread, so the adds stay in
+                    // program order (deterministic)
+                    atomicAdd(&p.kpart[(size_t(blockIdx.x) * S + s) * size_t(n) * 8 + lb * 8 + c], sum);
                 }
             }
             __syncthreads();
