@@ -167,6 +167,9 @@ constexpr size_t res_smem() {
            1024;
 }
 
+// N12: n == 12 (every group fully rotated): the phases are compile-time
+// instances (no runtime group/ops dispatch), like the streaming passes' programs.
+template <bool N12>
 __global__ void __launch_bounds__(kThreads, 2)
     resident_kernel(const __grid_constant__ ResidentParams p,
                     const __grid_constant__ CUtensorMap m_psi0,
@@ -269,13 +272,21 @@ __global__ void __launch_bounds__(kThreads, 2)
         for (int s = 0; s < S; ++s) {
             const PhaseEnv e = env_for(s);
             if (s + 1 < S) load_stage(s + 1); // other slot: its latency overlaps this stage
-            run_phase_fwd(0, pt, tid, 2u | 4u, e);
-            __syncthreads();
-            if (rot & 0xF0u) {
-                run_phase_fwd(1, pt, tid, 4u, e);
+            if constexpr (N12) {
+                phase_fwd<0, 6u, true>(pt, tid, e);
                 __syncthreads();
+                phase_fwd<1, 4u, true>(pt, tid, e);
+                __syncthreads();
+                phase_fwd<2, 4u, true>(pt, tid, e);
+            } else {
+                run_phase_fwd(0, pt, tid, 2u | 4u, e);
+                __syncthreads();
+                if (rot & 0xF0u) {
+                    run_phase_fwd(1, pt, tid, 4u, e);
+                    __syncthreads();
+                }
+                if (rot & 0xF00u) run_phase_fwd(2, pt, tid, 4u, e);
             }
-            if (rot & 0xF00u) run_phase_fwd(2, pt, tid, 4u, e);
             const bool slot = ((s + 1) % p.ckpt == 0) && (s + 1 < S) && !p.forward_only;
             if (slot) fence_async_smem();
             __syncthreads();
@@ -343,15 +354,23 @@ __global__ void __launch_bounds__(kThreads, 2)
             }
             const PhaseEnv e = env_for(s);
             if (s > 0) load_stage(s - 1); // other slot: its latency overlaps this stage
-            if (rot & 0xF00u) {
-                run_phase_bwd(2, pt, lt, tid, 4u, e);
+            if constexpr (N12) {
+                phase_bwd<2, 4u, true>(pt, lt, tid, e);
                 __syncthreads();
-            }
-            if (rot & 0xF0u) {
-                run_phase_bwd(1, pt, lt, tid, 4u, e);
+                phase_bwd<1, 4u, true>(pt, lt, tid, e);
                 __syncthreads();
+                phase_bwd<0, 6u, true>(pt, lt, tid, e);
+            } else {
+                if (rot & 0xF00u) {
+                    run_phase_bwd(2, pt, lt, tid, 4u, e);
+                    __syncthreads();
+                }
+                if (rot & 0xF0u) {
+                    run_phase_bwd(1, pt, lt, tid, 4u, e);
+                    __syncthreads();
+                }
+                run_phase_bwd(0, pt, lt, tid, 4u | 2u, e);
             }
-            run_phase_bwd(0, pt, lt, tid, 4u | 2u, e);
             __syncthreads();
             if (tid < 96) {
                 const int lb = tid >> 3, c = tid & 7;
@@ -383,13 +402,15 @@ size_t resident_smem_bytes() { return res_smem(); }
 
 int resident_occupancy() {
     if (!g_attrs) {
-        if (cudaFuncSetAttribute(resident_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        if (cudaFuncSetAttribute(resident_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(res_smem())) != cudaSuccess ||
+            cudaFuncSetAttribute(resident_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  int(res_smem())) != cudaSuccess)
             return 0;
         g_attrs = true;
     }
     int blocks = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, resident_kernel, kThreads, res_smem());
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, resident_kernel<false>, kThreads, res_smem());
     return blocks;
 }
 
@@ -397,7 +418,10 @@ cudaError_t launch_resident(cudaStream_t st, int grid, const ResidentParams &p,
                             const CUtensorMap *psi0, const CUtensorMap *slots_map,
                             const CUtensorMap *out_map) {
     if (resident_occupancy() <= 0) return cudaErrorInvalidConfiguration;
-    resident_kernel<<<grid, kThreads, res_smem(), st>>>(p, *psi0, *slots_map, *out_map);
+    if (p.n == 12)
+        resident_kernel<true><<<grid, kThreads, res_smem(), st>>>(p, *psi0, *slots_map, *out_map);
+    else
+        resident_kernel<false><<<grid, kThreads, res_smem(), st>>>(p, *psi0, *slots_map, *out_map);
     return cudaGetLastError();
 }
 
