@@ -436,6 +436,7 @@ void enqueue_fused(qf_plan *pl, const double *theta_dev, double *out_dev, qf_sta
         r.ry = pl->ry;
         r.dt = pl->dtab;
         r.cztabs = pl->cztab;
+        r.cz_stride = int(P.layouts.size());
         r.stage_cz = pl->stage_cz;
         r.wfinal = pl->wfinal;
         r.czfinal = pl->final_adj;

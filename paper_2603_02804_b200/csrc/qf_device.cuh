@@ -384,12 +384,14 @@ struct PhaseEnv {
     const float4 *rys; // smem [2][12] ry_entry(): round 0, round 1
     const float2 *mgs; // smem [2][3] group scales (M, M): round 0, round 1
     uint32_t rot;
-    bool scale;        // apply the group scales (false: folded into the diagonal)
+    bool scale;        // round 0: apply the group scales (false: folded into the diagonal)
+    bool scale1;       // the same for round 1 (rounds of two stages may differ)
     DiagCtx d;
     const float2 *treg_s;
     const float *kc;   // smem [2][3] K scale corrections (nullptr = 1)
     uint32_t zm;       // bit r: round r measures Z (stage 0 only; zchain_kernel)
-    double *acc_w;     // this warp's [2 rounds][12][8] accumulators
+    double *acc_w;     // this warp's [12][8] accumulators of round 0
+    double *acc_w1;    // ... and of round 1
 };
 __device__ __forceinline__ float kcorr(const PhaseEnv &e, int r, int g) {
     return e.kc ? e.kc[3 * r + g] : 1.f;
@@ -402,7 +404,7 @@ __device__ __forceinline__ void phase_fwd(uint8_t *tile, uint32_t tau, const Pha
     lds16<G>(tile, tau, v);
     if (OPS & 1u) ry_round<G, false, FULL>(v, e.rys, e.rot, e.mgs[G], e.scale);
     if (OPS & 2u) apply_diag<false>(v, e.d, e.treg_s);
-    if (OPS & 4u) ry_round<G, false, FULL>(v, e.rys + 12, e.rot, e.mgs[3 + G], e.scale);
+    if (OPS & 4u) ry_round<G, false, FULL>(v, e.rys + 12, e.rot, e.mgs[3 + G], e.scale1);
     sts16<G>(tile, tau, v);
 }
 template <int G, uint32_t OPS, bool FULL, bool RTZ = true>
@@ -421,10 +423,10 @@ __device__ __forceinline__ void phase_bwd(uint8_t *pt, uint8_t *lt, uint32_t tau
     return;
 #endif
     if (OPS & 4u) {
-        ry_round<G, true, FULL>(p, e.rys + 12, e.rot, e.mgs[3 + G], e.scale);
-        ry_round<G, true, FULL>(l, e.rys + 12, e.rot, e.mgs[3 + G], e.scale);
-        if (RTZ && (e.zm & 2u)) kmeasure<G, FULL, true>(p, l, e.rot, e.acc_w + 12 * 8, kcorr(e, 1, G));
-        else kmeasure<G, FULL, false>(p, l, e.rot, e.acc_w + 12 * 8, kcorr(e, 1, G));
+        ry_round<G, true, FULL>(p, e.rys + 12, e.rot, e.mgs[3 + G], e.scale1);
+        ry_round<G, true, FULL>(l, e.rys + 12, e.rot, e.mgs[3 + G], e.scale1);
+        if (RTZ && (e.zm & 2u)) kmeasure<G, FULL, true>(p, l, e.rot, e.acc_w1, kcorr(e, 1, G));
+        else kmeasure<G, FULL, false>(p, l, e.rot, e.acc_w1, kcorr(e, 1, G));
     }
     if (OPS & 2u) {
         apply_diag<true>(p, e.d, e.treg_s);

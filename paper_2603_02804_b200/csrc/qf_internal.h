@@ -117,8 +117,9 @@ struct ResidentParams {
     uint32_t y_count;
     const float2 *ry;          // [stages][n]
     const DiagTab *dt;         // [stages]
-    const CzTab *cztabs;       // distinct CZ sets in the resident layout
-    const int *stage_cz;       // [stages] -> cztabs index or -1
+    const CzTab *cztabs;       // [CZ set][cz_stride] tables (per resident layout)
+    int cz_stride;             // resident layouts: 1, or 2 for n = 12 (diagonal in group 0 / 2)
+    const int *stage_cz;       // [stages] -> CZ set index or -1
     const double *wfinal;      // [n] final diagonal phases
     const CzAdj *czfinal;      // nullptr = none
     double *kpart;             // [grid][stages][n][8]

@@ -128,10 +128,12 @@ __global__ void __launch_bounds__(kThreads, min_blocks(BWD, NB))
     env.mgs = mgs;
     env.rot = p.rot_mask;
     env.scale = scale;
+    env.scale1 = scale;
     env.treg_s = treg_s;
     env.kc = BWD ? kc : nullptr;
     env.zm = uint32_t(p.zmask);
     env.acc_w = acc + warp * 2 * 12 * 8;
+    env.acc_w1 = env.acc_w + 12 * 8;
     env.d.base = make_float2(1.f, 0.f);
     env.d.sgn = 0;
     int it = 0;
@@ -257,10 +259,12 @@ __global__ void __launch_bounds__(kDualThreads, 1)
     env.mgs = mgs;
     env.rot = p.rot_mask;
     env.scale = scale;
+    env.scale1 = scale;
     env.treg_s = treg_s;
     env.kc = kc;
     env.zm = uint32_t(p.zmask);
     env.acc_w = acc + warp * 2 * 12 * 8;
+    env.acc_w1 = env.acc_w + 12 * 8;
     env.d.base = make_float2(1.f, 0.f);
     env.d.sgn = 0;
     const int bar_id = 1 + half;

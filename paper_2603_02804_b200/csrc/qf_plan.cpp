@@ -185,6 +185,12 @@ Plan make_plan(const qf_gate *gates, size_t n_gates, uint32_t n, uint32_t n_para
         R.gd = 0;
         finish_layout(R);
         plan.layouts.push_back(R);
+        if (n == 12) { // chained stages (qf_resident.cu): odd stages apply D in group 2
+            PassLayout R2 = R;
+            R2.gd = 2;
+            finish_layout(R2);
+            plan.layouts.push_back(R2);
+        }
     } else {
         PassLayout A;
         A.row_start = 4;
@@ -259,6 +265,8 @@ Plan make_plan(const qf_gate *gates, size_t n_gates, uint32_t n, uint32_t n_para
     // every layout has finished stage dnext-1 it also applies D_{dnext} and, on
     // its own qubits, Ry_{dnext}. Two layouts -> one pass per stage.
     plan.stage_layout.assign(S, 0);
+    if (plan.resident && n == 12)
+        for (int t = 0; t < S; ++t) plan.stage_layout[t] = t & 1;
     if (!plan.resident && S > 0) {
         std::vector<int> r(NL, 0);
         int dnext = 0, X = 0;

@@ -249,14 +249,87 @@ __global__ void __launch_bounds__(kThreads, 2)
         e.mgs = mgs + sl * 6;
         e.rot = rot;
         e.scale = !fold[sl];
+        e.scale1 = e.scale;
         e.kc = kc + sl * 6;
         e.zm = s == 0 ? 3u : 0u; // Z at stage 0 only (zchain_kernel rebuilds the rest)
         e.treg_s = treg_s + sl * 16;
         e.acc_w = acc + warp * 2 * 12 * 8;
+        e.acc_w1 = e.acc_w + 12 * 8;
         const int c = p.stage_cz[s];
-        const CzTab *cz = c >= 0 ? p.cztabs + c : nullptr;
+        const CzTab *cz = c >= 0 ? p.cztabs + c * p.cz_stride : nullptr;
         e.d = diag_ctx(tid, p.dt[s].tthr[tid], cz ? cz->thrinfo[tid] : 0u, p.dt + s, cz, nullptr, 0u);
         return e;
+    };
+
+    // ---- n = 12: chained stages, 2 shared-memory phases per stage instead of 3.
+    // Stage s runs its Ry rounds on groups f(s), 1, l(s) with f(s) = 0 (s even) or
+    // 2 (s odd) and l(s) = 2 - f(s); the phase that ends stage s-1 on group
+    // l(s-1) = f(s) goes straight on with D_s and Ry_s there (the streaming
+    // passes' pairing, qf_plan.cpp), split only where a checkpoint slot sits
+    // between the two stages. D_s is tabulated in group f(s)'s orientation
+    // (resident layouts 0 / 1, stage_layout = s & 1). Stage data live in a 4-entry
+    // ring (stage s in entries s&1 and (s&1)+2), so the round-0 (stage a) and
+    // round-1 (stage a+1) data of a phase are adjacent entries; K of stage s
+    // accumulates in slot s&1. kc follows the stage's own group order.
+    auto load12 = [&](int s) {
+        const int e0 = s & 1, first = (s & 1) ? 2 : 0, last = 2 - first;
+        auto gscale = [&](int g) {
+            float M = 1.f;
+            for (int b = 0; b < 4; ++b) M *= ry_entry(p.ry[size_t(s) * 12 + 4 * g + b]).z;
+            return M;
+        };
+        if (tid >= 64 && tid < 76) {
+            const int lb = tid - 64;
+            const float4 v = ry_entry(p.ry[size_t(s) * 12 + lb]);
+            rys[e0 * 12 + lb] = v;
+            rys[(e0 + 2) * 12 + lb] = v;
+        } else if (tid >= 76 && tid < 92) {
+            const float M[3] = {gscale(0), gscale(1), gscale(2)};
+            const float F = M[0] * M[1] * M[2];
+            const bool f = F >= 0x1p-40f;
+            float2 t = p.dt[s].treg[tid - 76];
+            if (f) t = make_float2(t.x * F, t.y * F);
+            treg_s[(s & 1) * 16 + (tid - 76)] = t;
+            if (tid == 76) {
+                for (int e = e0; e < 4; e += 2) {
+                    fold[e] = f;
+                    kc[e * 3 + last] = f ? M[last] * M[last] : 1.f;
+                    kc[e * 3 + 1] = f ? (M[last] * M[1]) * (M[last] * M[1]) : 1.f;
+                    kc[e * 3 + first] = f ? F * F : 1.f;
+                }
+            }
+        } else if (tid >= 92 && tid < 95) {
+            const int g = tid - 92;
+            const float M = gscale(g);
+            mgs[e0 * 3 + g] = make_float2(M, M);
+            mgs[(e0 + 2) * 3 + g] = make_float2(M, M);
+        }
+    };
+    // round 0 = stage a (a = -1: none), round 1 = stage a + 1, diagonal of stage d (-1: none)
+    auto env12 = [&](int a, int d) {
+        PhaseEnv e;
+        const int b = a & 1;
+        e.rys = rys + b * 12;
+        e.mgs = mgs + b * 3;
+        e.kc = kc + b * 3;
+        e.rot = 0xFFFu;
+        e.scale = !fold[b];
+        e.scale1 = !fold[b + 1];
+        e.zm = (a == 0 ? 1u : 0u) | (a + 1 == 0 ? 2u : 0u);
+        e.acc_w = acc + warp * 2 * 12 * 8 + (a & 1) * 96;
+        e.acc_w1 = acc + warp * 2 * 12 * 8 + ((a + 1) & 1) * 96;
+        e.treg_s = treg_s + (d & 1) * 16;
+        e.d.base = make_float2(1.f, 0.f);
+        e.d.sgn = 0;
+        if (d >= 0) {
+            const int c = p.stage_cz[d];
+            const CzTab *cz = c >= 0 ? p.cztabs + c * p.cz_stride + (d & 1) : nullptr;
+            e.d = diag_ctx(tid, p.dt[d].tthr[tid], cz ? cz->thrinfo[tid] : 0u, p.dt + d, cz, nullptr, 0u);
+        }
+        return e;
+    };
+    auto slot_after = [&](int s) { // a checkpoint slot holds the state after stage s
+        return ((s + 1) % p.ckpt == 0) && (s + 1 < S) && !p.forward_only;
     };
 
     for (int t = blockIdx.x; t < p.tiles; t += gridDim.x) {
@@ -264,21 +337,52 @@ __global__ void __launch_bounds__(kThreads, 2)
             mbar_expect_tx(&mbar[0], kTileBytes);
             tma_load3(pt, &m_psi0, &mbar[0], 0, t * 256, 0);
         }
-        if (S > 0) load_stage(0);
+        if (S > 0) {
+            if constexpr (N12) load12(0);
+            else load_stage(0);
+        }
         mbar_wait(&mbar[0], phase);
         phase ^= 1u;
         __syncthreads();
         // ---------------- forward over all stages
-        for (int s = 0; s < S; ++s) {
-            const PhaseEnv e = env_for(s);
-            if (s + 1 < S) load_stage(s + 1); // other slot: its latency overlaps this stage
-            if constexpr (N12) {
-                phase_fwd<0, 6u, true>(pt, tid, e);
+        if constexpr (N12) {
+            for (int s = 0; s < S; ++s) {
+                const bool merged = s > 0 && !slot_after(s - 1);
+                { // head: group f(s): [Ry_{s-1}] D_s Ry_s
+                    const PhaseEnv e = env12(s - 1, s);
+                    if (s & 1) {
+                        if (merged) phase_fwd<2, 7u, true>(pt, tid, e);
+                        else phase_fwd<2, 6u, true>(pt, tid, e);
+                    } else {
+                        if (merged) phase_fwd<0, 7u, true>(pt, tid, e);
+                        else phase_fwd<0, 6u, true>(pt, tid, e);
+                    }
+                }
                 __syncthreads();
-                phase_fwd<1, 4u, true>(pt, tid, e);
+                if (s + 1 < S) load12(s + 1); // stage s-1's ring entries are free now
+                phase_fwd<1, 4u, true>(pt, tid, env12(s - 1, -1));
                 __syncthreads();
-                phase_fwd<2, 4u, true>(pt, tid, e);
-            } else {
+                const bool slot = slot_after(s);
+                if (s == S - 1 || slot) { // tail: Ry_s on group l(s) alone
+                    const PhaseEnv e = env12(s - 1, -1);
+                    if (s & 1) phase_fwd<0, 4u, true>(pt, tid, e);
+                    else phase_fwd<2, 4u, true>(pt, tid, e);
+                    if (slot) fence_async_smem();
+                    __syncthreads();
+                    if (slot) {
+                        if (tid == 0) {
+                            tma_store3(&m_slots, pt, 0, t * 256, (s + 1) / p.ckpt - 1);
+                            bulk_commit();
+                            bulk_wait_read0();
+                        }
+                        __syncthreads();
+                    }
+                }
+            }
+        } else {
+            for (int s = 0; s < S; ++s) {
+                const PhaseEnv e = env_for(s);
+                if (s + 1 < S) load_stage(s + 1); // other slot: its latency overlaps this stage
                 run_phase_fwd(0, pt, tid, 2u | 4u, e);
                 __syncthreads();
                 if (rot & 0xF0u) {
@@ -286,17 +390,17 @@ __global__ void __launch_bounds__(kThreads, 2)
                     __syncthreads();
                 }
                 if (rot & 0xF00u) run_phase_fwd(2, pt, tid, 4u, e);
-            }
-            const bool slot = ((s + 1) % p.ckpt == 0) && (s + 1 < S) && !p.forward_only;
-            if (slot) fence_async_smem();
-            __syncthreads();
-            if (slot) {
-                if (tid == 0) {
-                    tma_store3(&m_slots, pt, 0, t * 256, (s + 1) / p.ckpt - 1);
-                    bulk_commit();
-                    bulk_wait_read0();
-                }
+                const bool slot = slot_after(s);
+                if (slot) fence_async_smem();
                 __syncthreads();
+                if (slot) {
+                    if (tid == 0) {
+                        tma_store3(&m_slots, pt, 0, t * 256, (s + 1) / p.ckpt - 1);
+                        bulk_commit();
+                        bulk_wait_read0();
+                    }
+                    __syncthreads();
+                }
             }
         }
         if (p.forward_only) { // fold D_f and store the final state
@@ -341,44 +445,15 @@ __global__ void __launch_bounds__(kThreads, 2)
             if (sample < p.batch) p.expect[sample] = es[ls << (n < 12 ? n : 12)];
         }
         // ---------------- backward
-        if (S > 0) load_stage(S - 1);
-        __syncthreads();
-        for (int s = S - 1; s >= 0; --s) {
-            if (((s + 1) % p.ckpt == 0) && (s + 1 < S)) { // re-anchor psi at the slot
-                if (tid == 0) {
-                    mbar_expect_tx(&mbar[0], kTileBytes);
-                    tma_load3(pt, &m_slots, &mbar[0], 0, t * 256, (s + 1) / p.ckpt - 1);
-                }
-                mbar_wait(&mbar[0], phase);
-                phase ^= 1u;
-            }
-            const PhaseEnv e = env_for(s);
-            if (s > 0) load_stage(s - 1); // other slot: its latency overlaps this stage
-            if constexpr (N12) {
-                phase_bwd<2, 4u, true>(pt, lt, tid, e);
-                __syncthreads();
-                phase_bwd<1, 4u, true>(pt, lt, tid, e);
-                __syncthreads();
-                phase_bwd<0, 6u, true>(pt, lt, tid, e);
-            } else {
-                if (rot & 0xF00u) {
-                    run_phase_bwd(2, pt, lt, tid, 4u, e);
-                    __syncthreads();
-                }
-                if (rot & 0xF0u) {
-                    run_phase_bwd(1, pt, lt, tid, 4u, e);
-                    __syncthreads();
-                }
-                run_phase_bwd(0, pt, lt, tid, 4u | 2u, e);
-            }
-            __syncthreads();
+        // K of stage s from accumulator slot ks, added (RED) to this CTA's kpart row
+        auto flush_k = [&](int s, int ks) {
             if (tid < 96) {
                 const int lb = tid >> 3, c = tid & 7;
                 if (lb < n) {
                     double sum = 0.0;
 #pragma unroll
                     for (int w = 0; w < 8; ++w) {
-                        double *a = acc + ((w * 2 + 1) * 12 + lb) * 8 + c;
+                        double *a = acc + ((w * 2 + ks) * 12 + lb) * 8 + c;
                         sum += *a;
                         *a = 0.0;
                     }
@@ -388,7 +463,64 @@ __global__ void __launch_bounds__(kThreads, 2)
                     atomicAdd(&p.kpart[(size_t(blockIdx.x) * S + s) * size_t(n) * 8 + lb * 8 + c], sum);
                 }
             }
+        };
+        auto reanchor = [&](int s) { // psi := the forward state after stage s (slot)
+            if (tid == 0) {
+                mbar_expect_tx(&mbar[0], kTileBytes);
+                tma_load3(pt, &m_slots, &mbar[0], 0, t * 256, (s + 1) / p.ckpt - 1);
+            }
+            mbar_wait(&mbar[0], phase);
+            phase ^= 1u;
+        };
+        if constexpr (N12) {
+            if (S > 0) load12(S - 1);
             __syncthreads();
+            for (int s = S - 1; s >= 0; --s) {
+                if (s == S - 1 || slot_after(s)) { // tail alone: undo Ry_s on group l(s)
+                    if (slot_after(s)) reanchor(s);
+                    const PhaseEnv e = env12(s - 1, -1);
+                    if (s & 1) phase_bwd<0, 4u, true>(pt, lt, tid, e);
+                    else phase_bwd<2, 4u, true>(pt, lt, tid, e);
+                    __syncthreads();
+                }
+                if (s > 0) load12(s - 1); // stage s+1's ring entries are free now
+                phase_bwd<1, 4u, true>(pt, lt, tid, env12(s - 1, -1));
+                __syncthreads();
+                { // head: group f(s): undo Ry_s, D_s [, Ry_{s-1}]
+                    const bool merged = s > 0 && !slot_after(s - 1);
+                    const PhaseEnv e = env12(s - 1, s);
+                    if (s & 1) {
+                        if (merged) phase_bwd<2, 7u, true>(pt, lt, tid, e);
+                        else phase_bwd<2, 6u, true>(pt, lt, tid, e);
+                    } else {
+                        if (merged) phase_bwd<0, 7u, true>(pt, lt, tid, e);
+                        else phase_bwd<0, 6u, true>(pt, lt, tid, e);
+                    }
+                }
+                __syncthreads();
+                flush_k(s, s & 1);
+                __syncthreads();
+            }
+        } else {
+            if (S > 0) load_stage(S - 1);
+            __syncthreads();
+            for (int s = S - 1; s >= 0; --s) {
+                if (slot_after(s)) reanchor(s);
+                const PhaseEnv e = env_for(s);
+                if (s > 0) load_stage(s - 1); // other slot: its latency overlaps this stage
+                if (rot & 0xF00u) {
+                    run_phase_bwd(2, pt, lt, tid, 4u, e);
+                    __syncthreads();
+                }
+                if (rot & 0xF0u) {
+                    run_phase_bwd(1, pt, lt, tid, 4u, e);
+                    __syncthreads();
+                }
+                run_phase_bwd(0, pt, lt, tid, 4u | 2u, e);
+                __syncthreads();
+                flush_k(s, 1);
+                __syncthreads();
+            }
         }
     }
     if (tid == 0) bulk_wait0();

@@ -73,6 +73,16 @@ def test_hea_20q(ctx, oracle, n, batch):
     _check(res, oracle.gradient(gates, n, npar, psi0, theta, pauli))
 
 
+@pytest.mark.parametrize("layers,k", [(1, 0), (2, 1), (5, 1), (6, 2), (6, 3), (9, 3), (9, 0)])
+def test_resident_n12_chained_stages(ctx, oracle, layers, k):
+    """n = 12 sample-resident kernel: stages chained two phases each (odd stages
+    with the diagonal in group 2), split at every checkpoint slot; odd and even
+    stage counts, slots after odd and even stages (k = 0: engine default)."""
+    gates, npar, theta, psi0, pauli = _hea_case(12, layers, 3, seed=40 + layers)
+    res = capi.gradient_c64(ctx, gates, 12, npar, layers, k, psi0, theta, pauli)
+    _check(res, oracle.gradient(gates, 12, npar, psi0, theta, pauli))
+
+
 @pytest.mark.parametrize("n,layers", [(6, 8), (14, 4)])
 @pytest.mark.parametrize("k", [1, 2, 4])
 def test_checkpoint_intervals(ctx, oracle, n, layers, k):
@@ -144,7 +154,7 @@ def test_errors(ctx):
         capi.Plan(ctx, g26, 26, np26, 1, 0, 1 << 12, C.parse_pauli("Z" * 26))
 
 
-@pytest.mark.parametrize("n,layers,batch", [(4, 3, 5), (12, 2, 2), (14, 2, 2), (17, 2, 1)])
+@pytest.mark.parametrize("n,layers,batch", [(4, 3, 5), (12, 2, 2), (12, 5, 3), (14, 2, 2), (17, 2, 1)])
 def test_forward_state_matches_reference(ctx, ref, n, layers, batch):
     """Final state of the fused forward vs the reference's forward<double>,
     up to one global phase per sample (the device drops e^{i delta})."""
