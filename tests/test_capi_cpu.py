@@ -42,3 +42,17 @@ def test_library_is_sm100a_only():
                          text=True).stdout
     assert "sm_100a" in out
     assert "sm_90" not in out and "sm_80" not in out
+
+
+def test_group_api_without_device():
+    """The single-process multi-GPU entry points fail cleanly without a GPU
+    (no crash, no CPU fallback): invalid n_gpus is rejected before any device
+    or NCCL work; on the GPU box a real group is covered by test_gpu_multi."""
+    lib = pkg.load()
+    h = ctypes.c_void_p()
+    assert lib.qf_group_create(0, None, ctypes.byref(h)) in (pkg.capi.QF_EINVAL, pkg.capi.QF_EDEVICE)
+    assert lib.qf_last_error()
+    assert lib.qf_group_size(None) == 0
+    assert lib.qf_group_destroy(None) == 0
+    st = pkg.capi.QfStats()
+    assert lib.qf_plan_last_stats(None, ctypes.byref(st)) == pkg.capi.QF_EINVAL
