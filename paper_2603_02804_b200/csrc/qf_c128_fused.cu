@@ -178,10 +178,17 @@ __global__ void __launch_bounds__(kT, 2) seg_c128(const C128Seg sg, const C128Op
             if (i < 16) lq[i] = sg.lq[i];
         }
     }
+    // the segment's ops, section unitaries and CZ pairs, staged once per CTA
+    __shared__ C128Op ops_s[kC128MaxOps];
+    __shared__ double2 u_s[kC128MaxSec * 4];
+    __shared__ uint32_t cz_s[kC128MaxCzPairs];
+    const uint32_t nops = sg.op_end - sg.op_begin;
+    for (uint32_t i = tid; i < nops; i += kT) ops_s[i] = ops[sg.op_begin + i];
+    for (uint32_t i = tid; i < sg.nsec * 4; i += kT) u_s[i] = secU[size_t(sg.sec_begin) * 4 + i];
+    for (uint32_t i = tid; i < sg.cz_count; i += kT) cz_s[i] = czp[sg.cz_begin + i];
     if (BWD)
         for (uint32_t i = tid; i < sg.nsec * 64; i += kT) acc[i] = 0.0;
     __syncthreads();
-    const uint32_t nops = sg.op_end - sg.op_begin;
     constexpr int KA = (1 << kC128TileBits) / kT; // amplitudes per thread
     // local part of the global index of this thread's amplitudes (fixed per segment)
     uint32_t xl[KA];
@@ -196,14 +203,14 @@ __global__ void __launch_bounds__(kT, 2) seg_c128(const C128Seg sg, const C128Op
     uint32_t qlb[KA];
 #pragma unroll
     for (int k = 0; k < KA; ++k) qlb[k] = 0;
-    for (uint32_t i = sg.op_begin; i < sg.op_end; ++i) {
-        const C128Op op = ops[i];
+    for (uint32_t i = 0; i < nops; ++i) {
+        const C128Op op = ops_s[i];
         if (op.type != 1) continue;
 #pragma unroll
         for (int k = 0; k < KA; ++k) {
             uint32_t f = 0;
             for (uint32_t c = 0; c < op.b; ++c) {
-                const uint32_t w = czp[op.a + c];
+                const uint32_t w = cz_s[op.a - sg.cz_begin + c];
                 f ^= (xl[k] >> (w & 255u)) & (xl[k] >> (w >> 8)) & 1u;
             }
             qlb[k] |= f << op.q;
@@ -243,9 +250,9 @@ __global__ void __launch_bounds__(kT, 2) seg_c128(const C128Seg sg, const C128Op
         __syncthreads();
         if (t + gridDim.x < tiles) fetch(t + gridDim.x, buf ^ 1u);
         for (uint32_t ii = 0; ii < nops; ++ii) {
-            const C128Op op = ops[BWD ? sg.op_end - 1 - ii : sg.op_begin + ii];
+            const C128Op op = ops_s[BWD ? nops - 1 - ii : ii];
             if (op.type == 0 && ii + 1 < nops && amps >= 4) {
-                const C128Op op2 = ops[BWD ? sg.op_end - 2 - ii : sg.op_begin + ii + 1];
+                const C128Op op2 = ops_s[BWD ? nops - 2 - ii : ii + 1];
                 if (op2.type == 0 && op2.q != op.q) {
                     // two sections on different qubits in one round: each thread
                     // owns a quad (bits p1, p2) and applies (or undoes) op then op2
@@ -253,7 +260,7 @@ __global__ void __launch_bounds__(kT, 2) seg_c128(const C128Seg sg, const C128Op
                     // (K of a qubit is invariant under gates on other qubits)
                     const uint32_t p1 = uint32_t(lpos[op.q]), p2 = uint32_t(lpos[op2.q]);
                     const uint32_t lo = min(p1, p2), hi = max(p1, p2);
-                    const U2 ua = load_u(secU, op.a, BWD), ub = load_u(secU, op2.a, BWD);
+                    const U2 ua = load_u(u_s, op.a - sg.sec_begin, BWD), ub = load_u(u_s, op2.a - sg.sec_begin, BWD);
                     double ka[8] = {0, 0, 0, 0, 0, 0, 0, 0}, kb[8] = {0, 0, 0, 0, 0, 0, 0, 0};
                     if (tid < (amps >> 2)) { // amps / 4 <= kT: one quad per thread
                         const uint32_t b0 = insert0(insert0(tid, lo), hi);
@@ -302,7 +309,7 @@ __global__ void __launch_bounds__(kT, 2) seg_c128(const C128Seg sg, const C128Op
             }
             if (op.type == 0) { // a single section
                 const uint32_t pos = uint32_t(lpos[op.q]);
-                const U2 u = load_u(secU, op.a, BWD);
+                const U2 u = load_u(u_s, op.a - sg.sec_begin, BWD);
                 double k8[8] = {0, 0, 0, 0, 0, 0, 0, 0};
                 for (uint32_t p = tid; p < pairs; p += kT) {
                     const uint32_t i0 = sw(insert0(p, pos)), i1 = sw(insert0(p, pos) | (1u << pos));
@@ -326,7 +333,7 @@ __global__ void __launch_bounds__(kT, 2) seg_c128(const C128Seg sg, const C128Op
                 // Q(xl) of this thread's amplitudes is precomputed (qlb, bit op.q).
                 uint32_t qr = 0, M = 0;
                 for (uint32_t c = 0; c < op.b; ++c) {
-                    const uint32_t w = czp[op.a + c], a = w & 255u, b = w >> 8;
+                    const uint32_t w = cz_s[op.a - sg.cz_begin + c], a = w & 255u, b = w >> 8;
                     const uint32_t ra = (xr_cur >> a) & 1u, rb = (xr_cur >> b) & 1u;
                     qr ^= ra & rb;
                     M ^= (ra << b) ^ (rb << a);
@@ -425,7 +432,7 @@ C128Plan build_c128_plan(const qf_gate *gates, size_t n_gates, uint32_t n) {
     while (i < P.ops.size() || (P.ops.empty() && P.segs.empty())) {
         std::set<uint32_t> S;
         for (uint32_t q = 0; q < nbase; ++q) S.insert(q);
-        uint32_t nsec = 0, ncz = 0;
+        uint32_t nsec = 0, ncz = 0, ncp = 0, cz0 = 0;
         size_t j = i;
         for (; j < P.ops.size(); ++j) {
             const C128Op &op = P.ops[j];
@@ -433,9 +440,15 @@ C128Plan build_c128_plan(const qf_gate *gates, size_t n_gates, uint32_t n) {
             if (needs && !S.count(op.q) && S.size() + 1 > m) break;
             if (op.type == 0 && nsec == uint32_t(kC128MaxSec)) break;
             if (op.type == 1 && ncz == uint32_t(kC128MaxCz)) break;
+            if (j - i == size_t(kC128MaxOps)) break;
+            if (op.type == 1 && ncp + op.b > uint32_t(kC128MaxCzPairs)) break;
             if (needs) S.insert(op.q);
             if (op.type == 0) ++nsec;
-            if (op.type == 1) P.ops[j].q = ncz++; // index of the CZ run within its segment
+            if (op.type == 1) {
+                if (ncz == 0) cz0 = op.a;
+                P.ops[j].q = ncz++; // index of the CZ run within its segment
+                ncp += op.b;
+            }
         }
         for (uint32_t q = 0; S.size() < m; ++q) S.insert(q);
         C128Seg sg{};
@@ -445,6 +458,8 @@ C128Plan build_c128_plan(const qf_gate *gates, size_t n_gates, uint32_t n) {
         sg.op_end = uint32_t(j);
         sg.sec_begin = sec;
         sg.nsec = nsec;
+        sg.cz_begin = cz0; // the segment's CZ pairs are contiguous (appended in op order)
+        sg.cz_count = ncp;
         for (int q = 0; q < 32; ++q) sg.lpos[q] = -1;
         uint32_t l = 0, r = 0;
         for (uint32_t q = 0; q < n; ++q) {

@@ -214,6 +214,8 @@ cudaError_t launch_reduce_c128(cudaStream_t st, const double *gpart, int gblocks
 constexpr int kC128TileBits = 10;
 constexpr int kC128MaxSec = 32; // sections per segment (shared K accumulators)
 constexpr int kC128MaxCz = 32;  // CZ runs per segment (one bit each in a register mask)
+constexpr int kC128MaxOps = 64;    // ops per segment (staged in shared memory)
+constexpr int kC128MaxCzPairs = 128; // CZ pairs per segment (staged in shared memory)
 struct C128Op {
     uint32_t type; // 0 section, 1 CZ run, 2 CNOT
     uint32_t q;    // section qubit / CNOT target / CZ run index within its segment
@@ -221,7 +223,7 @@ struct C128Op {
     uint32_t b;    // CZ pair count
 };
 struct C128Seg {
-    uint32_t m, nrest, op_begin, op_end, sec_begin, nsec;
+    uint32_t m, nrest, op_begin, op_end, sec_begin, nsec, cz_begin, cz_count;
     int8_t lpos[32]; // qubit -> local bit, -1 if the qubit indexes tiles
     uint8_t lq[16];  // local bit -> qubit (ascending)
     uint8_t rq[32];  // tile bit -> qubit (ascending)
