@@ -299,9 +299,16 @@ __device__ __forceinline__ void kbit3_all(const float2 (&p)[16], const float2 (&
 // diagonals and with every gate on other qubits, so Z before Ry_s(q) equals Z
 // just after Ry_{s-1}(q) = cos(b) Z_{s-1} - sin(b) X_{s-1} (b = beta_{s-1}(q)),
 // rebuilt per qubit by zchain_kernel; only stage 0 measures Z.
+//
+// kslot != nullptr (compiled backward programs, (X, Y) only): the reduce-scatter
+// stops at 8-lane groups and each lane adds its value (index lane & 7, times kc)
+// to a per-thread fp32 register accumulator that lives across tiles
+// (kreg_flush at the end of the kernel), instead of an fp64 shared-memory
+// read-modify-write per tile.
 template <int G, bool FULL, bool WZ>
 __device__ __forceinline__ void kmeasure(const float2 (&p)[16], const float2 (&l)[16],
-                                         uint32_t rot, double *acc_w, float kc) {
+                                         uint32_t rot, double *acc_w, float kc,
+                                         float *kslot = nullptr) {
 #if QF_ABLATE_K
     return; // timing ablation only
 #endif
@@ -328,6 +335,10 @@ __device__ __forceinline__ void kmeasure(const float2 (&p)[16], const float2 (&l
             const float keep = up ? v[i + m] : v[i];
             v[i] = keep + __shfl_xor_sync(0xffffffffu, send, m);
         }
+    }
+    if (!WZ && kslot) {
+        *kslot = fmaf(v[0], kc, *kslot);
+        return;
     }
     float r = v[0];
 #pragma unroll
@@ -392,6 +403,7 @@ struct PhaseEnv {
     uint32_t zm;       // bit r: round r measures Z (stage 0 only; zchain_kernel)
     double *acc_w;     // this warp's [12][8] accumulators of round 0
     double *acc_w1;    // ... and of round 1
+    float *kreg;       // compiled backward programs: per-thread [2 rounds][3 groups]
 };
 __device__ __forceinline__ float kcorr(const PhaseEnv &e, int r, int g) {
     return e.kc ? e.kc[3 * r + g] : 1.f;
@@ -426,7 +438,7 @@ __device__ __forceinline__ void phase_bwd(uint8_t *pt, uint8_t *lt, uint32_t tau
         ry_round<G, true, FULL>(p, e.rys + 12, e.rot, e.mgs[3 + G], e.scale1);
         ry_round<G, true, FULL>(l, e.rys + 12, e.rot, e.mgs[3 + G], e.scale1);
         if (RTZ && (e.zm & 2u)) kmeasure<G, FULL, true>(p, l, e.rot, e.acc_w1, kcorr(e, 1, G));
-        else kmeasure<G, FULL, false>(p, l, e.rot, e.acc_w1, kcorr(e, 1, G));
+        else kmeasure<G, FULL, false>(p, l, e.rot, e.acc_w1, kcorr(e, 1, G), RTZ ? nullptr : e.kreg + 3 + G);
     }
     if (OPS & 2u) {
         apply_diag<true>(p, e.d, e.treg_s);
@@ -436,7 +448,7 @@ __device__ __forceinline__ void phase_bwd(uint8_t *pt, uint8_t *lt, uint32_t tau
         ry_round<G, true, FULL>(p, e.rys, e.rot, e.mgs[G], e.scale);
         ry_round<G, true, FULL>(l, e.rys, e.rot, e.mgs[G], e.scale);
         if (RTZ && (e.zm & 1u)) kmeasure<G, FULL, true>(p, l, e.rot, e.acc_w, kcorr(e, 0, G));
-        else kmeasure<G, FULL, false>(p, l, e.rot, e.acc_w, kcorr(e, 0, G));
+        else kmeasure<G, FULL, false>(p, l, e.rot, e.acc_w, kcorr(e, 0, G), RTZ ? nullptr : e.kreg + G);
     }
 #if QF_ABLATE_SMEM
     if (p[0].x == 1.2345f && l[3].y == 5.4321f) sts16<G>(pt, tau, p); // keep the math live

@@ -265,6 +265,25 @@ __global__ void __launch_bounds__(kDualThreads, 1)
     env.zm = uint32_t(p.zmask);
     env.acc_w = acc + warp * 2 * 12 * 8;
     env.acc_w1 = env.acc_w + 12 * 8;
+    // Compiled programs accumulate (X, Y) per lane in fp32 registers (kmeasure
+    // kslot) and move them into this warp's fp64 slots every 16 tiles and at the
+    // end, so no fp32 sum runs over more than 16 tile partials.
+    float kreg[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    env.kreg = kreg;
+    auto kreg_flush = [&] {
+        const uint32_t lane = tid & 31u;
+#pragma unroll
+        for (int i = 0; i < 6; ++i) {
+            float r = kreg[i];
+            r += __shfl_xor_sync(0xffffffffu, r, 8);
+            r += __shfl_xor_sync(0xffffffffu, r, 16);
+            const int rr = i / 3, g = i % 3, bit = int(lane >> 1), comp = int(lane & 1u);
+            if (lane < 8 && ((p.rot_mask >> (4 * g + bit)) & 1u))
+                acc[((warp * 2 + rr) * 12 + 4 * g + bit) * 8 + comp] += double(r);
+            kreg[i] = 0.f;
+        }
+    };
+    int kcount = 0;
     env.d.base = make_float2(1.f, 0.f);
     env.d.sgn = 0;
     const int bar_id = 1 + half;
@@ -309,6 +328,12 @@ __global__ void __launch_bounds__(kDualThreads, 1)
                 if (i == p.nph - 1) refill();
             }
         }
+        if constexpr (PROG != 0) {
+            if (++kcount == 16) {
+                kreg_flush();
+                kcount = 0;
+            }
+        }
         fence_async_smem();
         named_bar(bar_id, kThreads);
         if (gtid == 0) {
@@ -326,6 +351,7 @@ __global__ void __launch_bounds__(kDualThreads, 1)
         }
         bulk_wait0();
     }
+    if constexpr (PROG != 0) kreg_flush();
     __syncthreads();
     if (tid < 2 * 12 * 8) {
         const int r = tid / 96, lb = (tid / 8) % 12, c = tid & 7;
