@@ -283,7 +283,6 @@ __global__ void __launch_bounds__(kDualThreads, 1)
             kreg[i] = 0.f;
         }
     };
-    int kcount = 0;
     env.d.base = make_float2(1.f, 0.f);
     env.d.sgn = 0;
     const int bar_id = 1 + half;
@@ -329,10 +328,7 @@ __global__ void __launch_bounds__(kDualThreads, 1)
             }
         }
         if constexpr (PROG != 0) {
-            if (++kcount == 16) {
-                kreg_flush();
-                kcount = 0;
-            }
+            if (((k >> 1) & 15) == 15) kreg_flush(); // every 16 tiles of this half
         }
         fence_async_smem();
         named_bar(bar_id, kThreads);
