@@ -1,7 +1,9 @@
 """compute-sanitizer workload (run under memcheck / racecheck / synccheck):
-one fused gradient per path on small configurations — sample-resident (n = 10),
-streaming with the compiled programs and the generic kernels (n = 14, 16),
-MemSave slots, the per-gate and complex128 paths."""
+one fused gradient per path on small configurations — sample-resident (n = 10,
+and n = 12 with chained stages and checkpoint splits), streaming with the
+compiled programs (register K accumulation) and the generic kernels (n = 14, 16,
+20), MemSave slots, the per-gate path, complex128 fused segments (several
+segments, off-tile CNOT controls) and per-gate, and a one-device NCCL group."""
 import os
 import sys
 
@@ -12,8 +14,9 @@ import paper_2603_02804_b200 as qf  # noqa: E402
 from paper_2603_02804_b200 import circuits as C  # noqa: E402
 
 ctx = qf.Context(0)
-for n, layers, batch, k, storage in [(10, 4, 3, 2, "full"), (14, 4, 1, 2, "full"), (16, 4, 1, 2, "full"),
-                                     (16, 4, 1, 1, "memsave")]:
+for n, layers, batch, k, storage in [(10, 4, 3, 2, "full"), (12, 5, 2, 1, "full"), (12, 6, 2, 2, "full"),
+                                     (14, 4, 1, 2, "full"), (16, 4, 1, 2, "full"), (16, 4, 1, 1, "memsave"),
+                                     (20, 2, 1, 1, "full")]:
     gates, M = C.build_hea(n, layers)
     pauli = C.parse_pauli(C.repeated_ixyz_label(n))
     r = qf.gradient_c64(ctx, gates, n, M, layers, k, C.new_random_state(n, batch, 1),
@@ -25,4 +28,12 @@ qf.gradient_c64(ctx, gates, 9, M, 0, 0, C.new_random_state(9, 2, 1), C.random_pa
                 pergate=True)
 qf.gradient_c128(ctx, gates, 9, M, 0, 0, C.new_random_state(9, 2, 1, np.float64),
                  C.random_parameters(M, 2), pauli)
+gates, M = C.random_circuit(14, 80, 5)
+pauli = C.parse_pauli(C.repeated_ixyz_label(14))
+for pg in (False, True):
+    qf.gradient_c128(ctx, gates, 14, M, 0, 0, C.new_random_state(14, 2, 1, np.float64),
+                     C.random_parameters(M, 2), pauli, pergate=pg)
+gates, M = C.build_hea(6, 3)
+qf.gradient_c64_multi(1, gates, 6, M, 3, 1, C.new_random_state(6, 3, 1), C.random_parameters(M, 2),
+                      C.parse_pauli(C.repeated_ixyz_label(6)))
 print("sanitize workload ok")
