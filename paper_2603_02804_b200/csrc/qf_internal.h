@@ -79,9 +79,13 @@ constexpr uint32_t prog_encode(int nph, const PassPhase *ph, uint32_t rot_mask) 
 constexpr PassPhase kProgAPh[5] = {{2, 1}, {1, 1}, {0, 7}, {1, 4}, {2, 4}};
 constexpr PassPhase kProgB20Ph[3] = {{1, 1}, {2, 7}, {1, 4}};
 constexpr PassPhase kProgB16Ph[1] = {{2, 7}};
+// n = 16 with the column group moved to layout B (qf_plan.cpp): A runs kProgB20's
+// phases on groups 1, 2; B rotates groups 0 and 2.
+constexpr PassPhase kProgB16xPh[3] = {{0, 1}, {2, 7}, {0, 4}};
 constexpr uint32_t kProgA = prog_encode(5, kProgAPh, 0xFFFu);
 constexpr uint32_t kProgB20 = prog_encode(3, kProgB20Ph, 0xFF0u);
 constexpr uint32_t kProgB16 = prog_encode(1, kProgB16Ph, 0xF00u);
+constexpr uint32_t kProgB16x = prog_encode(3, kProgB16xPh, 0xF0Fu);
 
 struct PassParams {
     int n;

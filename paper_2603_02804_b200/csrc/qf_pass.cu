@@ -384,12 +384,14 @@ cudaError_t ensure_attrs() {
     if (e == cudaSuccess) e = set_smem(pass_kernel<false, 2, kProgA>, pass_smem(false, 2));
     if (e == cudaSuccess) e = set_smem(pass_kernel<false, 2, kProgB20>, pass_smem(false, 2));
     if (e == cudaSuccess) e = set_smem(pass_kernel<false, 2, kProgB16>, pass_smem(false, 2));
+    if (e == cudaSuccess) e = set_smem(pass_kernel<false, 2, kProgB16x>, pass_smem(false, 2));
     if (e == cudaSuccess) e = set_smem(pass_kernel<true, 1>, pass_smem(true, 1));
     if (e == cudaSuccess) e = set_smem(pass_kernel<true, 3>, pass_smem(true, 3));
     if (e == cudaSuccess) e = set_smem(pass_bwd_dual<0>, dual_smem());
     if (e == cudaSuccess) e = set_smem(pass_bwd_dual<kProgA>, dual_smem());
     if (e == cudaSuccess) e = set_smem(pass_bwd_dual<kProgB20>, dual_smem());
     if (e == cudaSuccess) e = set_smem(pass_bwd_dual<kProgB16>, dual_smem());
+    if (e == cudaSuccess) e = set_smem(pass_bwd_dual<kProgB16x>, dual_smem());
     g_attrs = e == cudaSuccess;
     return e;
 }
@@ -438,6 +440,7 @@ cudaError_t launch_pass(cudaStream_t st, bool backward, int grid, const PassPara
         if (prog == kProgA) pass_kernel<false, 2, kProgA><<<grid, kThreads, sm, st>>>(p, *psi_in, *psi_out, l);
         else if (prog == kProgB20) pass_kernel<false, 2, kProgB20><<<grid, kThreads, sm, st>>>(p, *psi_in, *psi_out, l);
         else if (prog == kProgB16) pass_kernel<false, 2, kProgB16><<<grid, kThreads, sm, st>>>(p, *psi_in, *psi_out, l);
+        else if (prog == kProgB16x) pass_kernel<false, 2, kProgB16x><<<grid, kThreads, sm, st>>>(p, *psi_in, *psi_out, l);
         else pass_kernel<false, 2><<<grid, kThreads, sm, st>>>(p, *psi_in, *psi_out, l);
     } else if (bwd_pipe() == 3) {
         pass_kernel<true, 3><<<grid, kThreads, pass_smem(true, 3), st>>>(p, *psi_in, *psi_out, l);
@@ -446,6 +449,7 @@ cudaError_t launch_pass(cudaStream_t st, bool backward, int grid, const PassPara
         if (prog == kProgA) pass_bwd_dual<kProgA><<<grid, kDualThreads, sm, st>>>(p, *psi_in, *psi_out, l);
         else if (prog == kProgB20) pass_bwd_dual<kProgB20><<<grid, kDualThreads, sm, st>>>(p, *psi_in, *psi_out, l);
         else if (prog == kProgB16) pass_bwd_dual<kProgB16><<<grid, kDualThreads, sm, st>>>(p, *psi_in, *psi_out, l);
+        else if (prog == kProgB16x) pass_bwd_dual<kProgB16x><<<grid, kDualThreads, sm, st>>>(p, *psi_in, *psi_out, l);
         else pass_bwd_dual<0><<<grid, kDualThreads, sm, st>>>(p, *psi_in, *psi_out, l);
     } else {
         pass_kernel<true, 1><<<grid, kThreads, pass_smem(true, 1), st>>>(p, *psi_in, *psi_out, l);

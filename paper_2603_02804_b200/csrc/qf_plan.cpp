@@ -220,6 +220,19 @@ Plan make_plan(const qf_gate *gates, size_t n_gates, uint32_t n, uint32_t n_para
             plan.layouts.push_back(P);
             hi = a;
         }
+        // 13 <= n <= 16: layout B rotates at most 4 row qubits (one phase) while A
+        // rotates 12 (five phases). Moving the column group's Ry (qubits 0..3)
+        // from A to B balances them at three phases each (same total work, but
+        // neither pass is left bound by one resource).
+        if (plan.layouts.size() == 2 && __builtin_popcount(plan.layouts[1].rot_mask) <= 4) {
+            PassLayout &LA = plan.layouts[0], &LB = plan.layouts[1];
+            LA.rot_mask = 0xFF0u;
+            LA.gd = 2;
+            LB.rot_mask |= 0x00Fu;
+            LB.gd = 2;
+            finish_layout(LA);
+            finish_layout(LB);
+        }
     }
     const int NL = static_cast<int>(plan.layouts.size());
 
