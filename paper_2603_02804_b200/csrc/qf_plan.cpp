@@ -224,8 +224,10 @@ Plan make_plan(const qf_gate *gates, size_t n_gates, uint32_t n, uint32_t n_para
         // rotates 12 (five phases). Moving the column group's Ry (qubits 0..3)
         // from A to B balances them at three phases each (same total work, but
         // neither pass is left bound by one resource).
-        if (plan.layouts.size() == 2 && __builtin_popcount(plan.layouts[1].rot_mask) <= 4) {
-            PassLayout &LA = plan.layouts[0], &LB = plan.layouts[1];
+        // (The same holds for the last layout at n = 21, 22: it rotates 1-2 qubits.)
+        if (plan.layouts.size() >= 2 && (plan.layouts.back().rot_mask & 0x0FFu) == 0 &&
+            __builtin_popcount(plan.layouts.back().rot_mask) <= 4) {
+            PassLayout &LA = plan.layouts[0], &LB = plan.layouts.back();
             LA.rot_mask = 0xFF0u;
             LA.gd = 2;
             LB.rot_mask |= 0x00Fu;
