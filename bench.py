@@ -209,13 +209,194 @@ def workload_config(args, wl):
 
 
 # ------------------------------------------------------------ GPU arm
-def run_ours(args):
+def fp32_peak():
+    fp = os.path.join(ROOT, "profiles", "fp32_peak.json")
+    return json.load(open(fp))["tfma_per_s"] if os.path.exists(fp) else 36.9
+
+
+def roofline_of(prof, steps, n, layers, B, workload):
+    """Roofline block of the dominant kernel kind of a timed region: algorithmic
+    bytes (or lane-FMA) per launch / its average CUDA-event launch time."""
+    peak, peak_src = measured_peaks()
+    kinds = {k: v for k, v in prof.items() if v["launches"]}
+    dom = max(kinds, key=lambda k: kinds[k]["ms"])
+    d = kinds[dom]
+    total_kernel_ms = sum(v["ms"] for v in kinds.values())
+    per_kind = {k: {"launches": v["launches"], "ms": v["ms"],
+                    "GBps": v["bytes"] / (v["ms"] / 1e3) / 1e9 if v["ms"] else None}
+                for k, v in kinds.items()}
+    if dom == "resident":
+        # sample-resident (n <= 12): FP32 CUDA-core bound (SURVEY §8d); per stage
+        # and amplitude: forward 2n (Ry, one FFMA2 per output) + 8 (diagonal),
+        # backward 4n (Ry on psi and lambda) + 6n (X, Y, Z per qubit) + 16 (diagonal)
+        per_amp = (2 * n + 8) + (10 * n + 16)
+        lane_fma = per_amp * B * (1 << n) * layers * steps
+        ach = lane_fma / (d["ms"] / 1e3) / 1e12
+        pk = fp32_peak()
+        return {"bound": "fp32", "kernel": dom, "achieved": ach, "peak": pk, "unit": "TFMA/s",
+                "frac": ach / pk, "traffic": None,
+                "peak_source": "tools/ffma_probe.cu on this pool (profiles/fp32_peak.json)",
+                "lane_fma_per_amp_stage": per_amp, "avg_launch_ms": d["ms"] / d["launches"],
+                "share_of_step": d["ms"] / max(total_kernel_ms, 1e-9), "per_kind": per_kind,
+                "hbm_GBps": d["bytes"] / (d["ms"] / 1e3) / 1e9}
+    achieved = d["bytes"] / (d["ms"] / 1e3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            traffic = json.load(f).get(f"{workload}:{dom}")
+    roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
+            "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+            "peak_source": peak_src,
+            "bytes_per_launch": d["bytes"] / d["launches"],
+            "avg_launch_ms": d["ms"] / d["launches"],
+            "share_of_step": d["ms"] / max(total_kernel_ms, 1e-9),
+            "per_kind": per_kind,
+            "algorithmic_bytes": "per state S = B*2^n*8; fwd pass 2S, bwd pass 4S (3S at a "
+                                 "checkpoint block start), observable 2S"}
+    # FP32 (CUDA-core) co-bound of the dominant pass kind (DESIGN.md §4): per
+    # amplitude per stage forward 2n + 8, backward 4n (Ry on psi, lambda) + 4n
+    # (X, Y; Z chained) + 16 (diagonal)
+    per_amp = {"backward_pass": 8 * n + 16, "forward_pass": 2 * n + 8}.get(dom)
+    if per_amp:
+        stages_per_launch = layers / max(1, d["launches"] / max(1, steps))
+        lane_fma = per_amp * B * (1 << n) * stages_per_launch
+        ach = lane_fma / (d["ms"] / d["launches"] / 1e3) / 1e12
+        pk = fp32_peak()
+        roof["fp32"] = {"achieved": ach, "peak": pk, "unit": "TFMA/s", "frac": ach / pk,
+                        "lane_fma_per_amp_stage": per_amp,
+                        "peak_source": "tools/ffma_probe.cu on this pool (profiles/fp32_peak.json)"}
+    return roof
+
+
+def measure(pkg, C, torch, dist, dev, rank, world, wl, batch_global, steps, warmup, storage,
+            scaling, e2e=False, refsig=False, clocks=False, workload="hea20q"):
+    """One workload: plan this rank's shard, warm up, time `steps` fused
+    gradients (+ the all-reduce) with CUDA events on the plan stream, max over
+    ranks. Returns (line fields, plan, dp) -- the caller closes them."""
     import numpy as np
+    from paper_2603_02804_b200.parallel import DataParallelGradient, shard_range
+    n, layers, k = wl["n"], wl["layers"], wl["ckpt"]
+    a, b = shard_range(batch_global, rank, world)
+    B = b - a
+    gates, M = C.build_hea(n, layers)
+    pauli = C.parse_pauli(C.repeated_ixyz_label(n))
+    ctx = pkg.Context(dev)
+    plan = pkg.Plan(ctx, gates, n, M, layers, k, B, pauli, storage=storage)
+    plan.random_psi0(SEED_STATE, first_sample=a)
+    theta_h = torch.from_numpy(C.random_parameters(M, SEED_THETA)).pin_memory()
+    theta_d = theta_h.to(f"cuda:{dev}")
+    dp = DataParallelGradient(plan, torch, dist if world > 1 else None)
+    stream = dp.stream
+    res = {}
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{dev}")
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(warmup):
+        dp.step_device(theta_d)
+    stream.synchronize()
+    launches_per_step = plan.gradient(theta_h.numpy()).stats["kernel_launches"]
+    plan.set_profiling(True)
+    plan.profile(reset=True)
+    sampler = ClockSampler(dev) if (rank == 0 and clocks) else None
+    barrier()
+    torch.cuda.synchronize()
+    if sampler:
+        sampler.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        dp.step_device(theta_d)
+    e1.record(stream)
+    stream.synchronize()
+    torch.cuda.synchronize()
+    if sampler:
+        res["clocks"] = sampler.stop()
+    barrier()
+    ms = max_over_ranks(e0.elapsed_time(e1))
+    prof = plan.profile(reset=True)
+    plan.set_profiling(False)
+    ms_per_step = ms / steps
+    res.update({"value": batch_global / (ms_per_step / 1000.0), "ms_per_step": ms_per_step,
+                "steps": steps, "warmup": warmup, "scaling": scaling,
+                "gpu_launches": int(launches_per_step * steps)})
+    out = dp.out[: M + 1].double().cpu().numpy()
+    assert np.all(np.isfinite(out)), "non-finite gradient"
+    res["roofline"] = roofline_of(prof, steps, n, layers, B, workload)
+    if n > 12:
+        # whole step against the BASELINE formula B_U = S(6Pd + d/k + 1), P = 2
+        peak, _ = measured_peaks()
+        P = 2
+        kk = k or min(layers, 10)
+        bu = (1 << n) * 8 * (6 * P * layers + layers / kk + 1) * B
+        res["roofline"]["step_formula_frac"] = bu / (ms_per_step / 1e3) / (peak * 1e9)
+        res["roofline"]["step_formula"] = ("B_U = S(6Pd + d/k + 1) with P=2 (BASELINE.md §2); "
+                                           "the paired-stage schedule moves P=1")
+
+    if e2e:
+        # end-to-end: host buffers, psi0 H2D (pinned) + theta H2D + gradient +
+        # all-reduce + D2H of [grad | loss] inside the timed region
+        psi_h = torch.empty(B * (2 << n), dtype=torch.float32).pin_memory()
+        plan.download_psi0_ptr(psi_h.data_ptr())
+        res_h = torch.empty(M + 1, dtype=torch.float64).pin_memory()
+        dp.step_host(psi_h, theta_h, theta_d, res_h)
+        stream.synchronize()
+        barrier()
+        torch.cuda.synchronize()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(steps):
+            dp.step_host(psi_h, theta_h, theta_d, res_h)
+        f1.record(stream)
+        stream.synchronize()
+        e2e_ms = max_over_ranks(f0.elapsed_time(f1)) / steps
+        res["e2e"] = {"value": batch_global / (e2e_ms / 1000.0), "unit": "samples/s",
+                      "h2d_bytes_per_step": int(psi_h.numel() * 4 + theta_h.numel() * 8),
+                      "d2h_bytes_per_step": int(res_h.numel() * 8), "ms_per_step": e2e_ms,
+                      "api": "capi.Plan.upload_psi0 + qf_plan_gradient_device + all-reduce + D2H"}
+        if refsig and world == 1:
+            # the reference-signature call: one-shot qf_gradient_c64 on PAGEABLE host
+            # buffers (what qfuse::b200::run_checkpointed / gradient<float> do per
+            # call, bench.cpp:114-133); the plan is cached in the context after the
+            # first call, psi0 staged through pinned memory by host threads
+            psi_np = psi_h.numpy().reshape(B, 1 << n, 2).copy()
+            th_np = theta_h.numpy().copy()
+            dp.close()
+            plan.close()
+            dp = plan = None
+            torch.cuda.empty_cache()
+            one = pkg.gradient_c64(ctx, gates, n, M, layers, k, psi_np, th_np, pauli,
+                                   storage=storage)  # builds + caches the plan
+            t0 = time.perf_counter()
+            for _ in range(steps):
+                one = pkg.gradient_c64(ctx, gates, n, M, layers, k, psi_np, th_np, pauli,
+                                       storage=storage)
+            rs_ms = (time.perf_counter() - t0) * 1000.0 / steps
+            assert np.isfinite(one.loss)
+            res["e2e_refsig"] = {
+                "value": batch_global / (rs_ms / 1000.0), "unit": "samples/s", "ms_per_step": rs_ms,
+                "h2d_bytes_per_step": int(psi_np.nbytes + th_np.nbytes),
+                "d2h_bytes_per_step": int((M + 1 + B) * 8),
+                "timer": "host wall clock around each synchronous call",
+                "api": "qf_gradient_c64_ex (one-shot C-ABI behind qfuse::b200::run_checkpointed), "
+                       "pageable numpy psi0/theta in, loss/grad/expect out"}
+    res["_n_per_rank"] = B
+    return res, ctx, plan, dp
+
+
+def run_ours(args):
     import torch
     import torch.distributed as dist
     import paper_2603_02804_b200 as pkg
     from paper_2603_02804_b200 import circuits as C
-    from paper_2603_02804_b200.parallel import DataParallelGradient
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -238,134 +419,67 @@ def run_ours(args):
         wl["layers"] = args.layers
     if args.ckpt is not None:
         wl["ckpt"] = args.ckpt
-    n, layers, B = wl["n"], wl["layers"], wl["batch"]
-    gates, M = C.build_hea(n, layers)
-    pauli = C.parse_pauli(C.repeated_ixyz_label(n))
-    ctx = pkg.Context(dev)
-    plan = pkg.Plan(ctx, gates, n, M, layers, wl["ckpt"], B, pauli, storage=args.storage)
-    plan.random_psi0(SEED_STATE, first_sample=rank * B)
-    theta_h = torch.from_numpy(C.random_parameters(M, SEED_THETA)).pin_memory()
-    theta_d = theta_h.to("cuda")
-    dp = DataParallelGradient(plan, torch, dist if world > 1 else None)
-    stream = dp.stream
-
-    def barrier():
-        if world > 1:
-            dist.barrier()
-
-    # warm-up
-    for _ in range(args.warmup):
-        dp.step_device(theta_d)
-    stream.synchronize()
-    launches_per_step = plan.gradient(theta_h.numpy()).stats["kernel_launches"]
-    plan.set_profiling(True)
-    plan.profile(reset=True)
-
-    sampler = ClockSampler(dev) if rank == 0 else None
-    barrier()
-    torch.cuda.synchronize()
-    if sampler:
-        sampler.start()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(args.steps):
-        dp.step_device(theta_d)
-    e1.record(stream)
-    stream.synchronize()
-    torch.cuda.synchronize()
-    clocks = sampler.stop() if sampler else None
-    barrier()
-    ms = e0.elapsed_time(e1)
-    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t.item())
-    prof = plan.profile(reset=True)
-    plan.set_profiling(False)
-    ms_per_step = ms / args.steps
-    value = world * B / (ms_per_step / 1000.0)
-
-    # result sanity (global loss / grad finite)
-    out = dp.out[: M + 1].double().cpu().numpy()
-    assert np.all(np.isfinite(out)), "non-finite gradient"
-
-    # ---- end-to-end leg: host buffers, copies inside the timed region
-    psi_h = torch.empty(B * (2 << n), dtype=torch.float32).pin_memory()
-    plan.download_psi0_ptr(psi_h.data_ptr())
-    res_h = torch.empty(M + 1, dtype=torch.float64).pin_memory()
-    dp.step_host(psi_h, theta_h, theta_d, res_h)
-    stream.synchronize()
-    barrier()
-    torch.cuda.synchronize()
-    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    f0.record(stream)
-    for _ in range(args.steps):
-        dp.step_host(psi_h, theta_h, theta_d, res_h)
-    f1.record(stream)
-    stream.synchronize()
-    e2e_ms = f0.elapsed_time(f1)
-    t = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    e2e_ms = float(t.item()) / args.steps
-    e2e = {"value": world * B / (e2e_ms / 1000.0), "unit": "samples/s",
-           "h2d_bytes_per_step": int(psi_h.numel() * 4 + theta_h.numel() * 8),
-           "d2h_bytes_per_step": int(res_h.numel() * 8), "ms_per_step": e2e_ms,
-           "api": "capi.Plan.upload_psi0 + qf_plan_gradient_device + NCCL all-reduce + D2H"}
-
-    # ---- roofline of the dominant kernel (backward pass in streaming mode)
-    peak, peak_src = measured_peaks()
-    kinds = {k: v for k, v in prof.items() if v["launches"]}
-    dom = max(kinds, key=lambda k: kinds[k]["ms"])
-    d = kinds[dom]
-    achieved = d["bytes"] / (d["ms"] / 1e3) / 1e9
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tp):
-        with open(tp) as f:
-            traffic = json.load(f).get(f"{args.workload}:{dom}")
-    total_kernel_ms = sum(v["ms"] for v in kinds.values())
-    roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
-                "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
-                "peak_source": peak_src,
-                "bytes_per_launch": d["bytes"] / d["launches"],
-                "avg_launch_ms": d["ms"] / d["launches"],
-                "share_of_step": d["ms"] / max(total_kernel_ms, 1e-9),
-                "per_kind": {k: {"launches": v["launches"], "ms": v["ms"],
-                                 "GBps": v["bytes"] / (v["ms"] / 1e3) / 1e9 if v["ms"] else None}
-                             for k, v in kinds.items()},
-                "algorithmic_bytes": "per state S = B*2^n*8; fwd pass 2S, bwd pass 4S (3S at a "
-                                     "checkpoint block start), observable 2S"}
-    # whole-step HBM fraction by the BASELINE formula B_U = S(6Pd + d/k + 1)
-    P = 2 if n > 12 else 1
-    k = wl["ckpt"] or min(layers, 10)
-    S = (1 << n) * 8
-    bu = S * (6 * P * layers + layers / k + 1) * B
-    roofline["step_formula_frac"] = bu / (ms_per_step / 1e3) / (peak * 1e9)
-    roofline["step_formula"] = f"B_U = S(6Pd + d/k + 1) with P={P} (BASELINE.md §2), our schedule moves P=1"
-    # FP32 (CUDA-core) roofline of the dominant kernel: the paired-pass kernels are
-    # FP32-bound. Algorithmic lane-FMA per amplitude per stage:
-    # forward 2n (one FFMA2 per output per qubit) + 8 (diag; group scales folded
-    # into it); backward 4n (Ry on psi and lambda) + 4n (X, Y; Z chained) + 16 (diag).
-    fp = os.path.join(ROOT, "profiles", "fp32_peak.json")
-    fp32_peak = json.load(open(fp))["tfma_per_s"] if os.path.exists(fp) else 36.9
-    per_amp = {"backward_pass": 8 * n + 16, "forward_pass": 2 * n + 8}.get(dom)
-    if per_amp and n > 12:
-        stages_per_launch = layers / max(1, d["launches"] / max(1, args.steps))
-        lane_fma = per_amp * B * (1 << n) * stages_per_launch
-        ach = lane_fma / (d["ms"] / d["launches"] / 1e3) / 1e12
-        roofline["fp32"] = {"achieved": ach, "peak": fp32_peak, "unit": "TFMA/s",
-                            "frac": ach / fp32_peak, "lane_fma_per_amp_stage": per_amp,
-                            "peak_source": "tools/ffma_probe.cu on this pool (profiles/fp32_peak.json)"}
-
+    n, layers = wl["n"], wl["layers"]
+    # weak: wl["batch"] samples per GPU; strong: wl["batch"] samples over all GPUs
+    batch_global = wl["batch"] * world if args.scaling == "weak" else wl["batch"]
+    res, ctx, plan, dp = measure(pkg, C, torch, dist, dev, rank, world, wl, batch_global,
+                                 args.steps, args.warmup, args.storage, args.scaling,
+                                 e2e=True, refsig=not args.no_refsig, clocks=True,
+                                 workload=args.workload)
+    B = res.pop("_n_per_rank")
+    cfg = workload_config(args, wl)
+    cfg["batch_per_gpu"] = B
+    cfg["global_batch"] = batch_global
     line = {
-        "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "metric": METRIC, "value": res["value"], "unit": "samples/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": res["ms_per_step"],
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (device SplitMix64/Box-Muller states seed 1234, theta seed 1235)",
-        "config": workload_config(args, wl), "clocks": clocks, "e2e": e2e,
-        "gpu_launches": int(launches_per_step * args.steps), "roofline": roofline,
+        "config": cfg, "clocks": res.get("clocks"), "e2e": res["e2e"],
+        "gpu_launches": res["gpu_launches"], "roofline": res["roofline"],
     }
+    if "e2e_refsig" in res:
+        line["e2e_refsig"] = res["e2e_refsig"]
+    for obj in (dp, plan, ctx):
+        if obj is not None:
+            obj.close()
+    del dp, plan, ctx
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+
+    # ---- secondary blocks: the other BASELINE configs on this box, each timed the
+    # same way with its own roofline (config 2 and 3 at N = 1; config 3 strong-scaled
+    # over the N GPUs of a scaling run)
+    if not args.no_secondary and args.workload == "hea20q" and not args.batch and not args.layers:
+        sec = {}
+        plans = [("hea16q", "full", "strong")]
+        if world == 1:
+            plans += [("hea12q", "full", "strong"), ("hea20q", "memsave", "weak")]
+        for name, storage, scaling in plans:
+            w2 = dict(WORKLOADS[name])
+            bg = w2["batch"] if scaling == "strong" else w2["batch"] * world
+            st = args.steps if name != "hea20q" else max(3, min(args.steps, 5))
+            try:
+                r2, c2, p2, d2 = measure(pkg, C, torch, dist, dev, rank, world, w2, bg, st,
+                                         max(3, args.warmup), storage, scaling, workload=name)
+            except Exception as exc:  # report, never hide the headline
+                sec[f"{name}_{storage}"] = {"error": str(exc)}
+                continue
+            for obj in (d2, p2, c2):
+                if obj is not None:
+                    obj.close()
+            del d2, p2, c2
+            torch.cuda.synchronize()
+            torch.cuda.empty_cache()
+            per = r2.pop("_n_per_rank")
+            r2["config"] = {"workload": f"{name}: HEA {w2['n']}q x {w2['layers']}L "
+                                        f"({w2['config']}), {bg} samples over {world} GPU(s)",
+                            "global_batch": bg, "batch_per_gpu": per, "ckpt_layers": w2["ckpt"],
+                            "storage": storage}
+            r2["unit"] = "samples/s"
+            sec[f"{name}" + ("_memsave" if storage == "memsave" else "")] = r2
+        line["secondary"] = sec
+
     # ---- CPU baseline: the reference on this host, rank 0 at N = 1 only
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
@@ -385,10 +499,7 @@ def run_ours(args):
         dist.barrier()
         dist.destroy_process_group()
     torch.cuda.synchronize()
-    sys.stdout.flush()
-    sys.stderr.flush()
-    # skip interpreter teardown: torch's allocator must not outlive the plan stream
-    os._exit(0)
+    return 0
 
 
 def main():
@@ -404,6 +515,13 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--storage", default="full", choices=["full", "memsave"],
                     help="StorageMode: memsave keeps checkpoint slots in bf16")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: --batch samples per GPU (config 4); strong: the workload's "
+                         "batch split over the GPUs (config 3)")
+    ap.add_argument("--no-secondary", action="store_true",
+                    help="skip the secondary workload blocks (hea16q, hea12q, memsave)")
+    ap.add_argument("--no-refsig", action="store_true",
+                    help="skip the reference-signature (one-shot C-ABI) e2e leg")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

@@ -92,6 +92,14 @@ int qf_ctx_create(int device, qf_ctx **out);
 int qf_ctx_destroy(qf_ctx *ctx);
 /* Optional HBM budget (bytes) checked before allocation; 0 = free memory. */
 int qf_ctx_set_hbm_limit(qf_ctx *ctx, uint64_t bytes);
+/* One-shot calls (qf_gradient_c64, _ex, _pergate_c64) keep their plan in the
+ * context and reuse it while the next call has the same gates, shape and
+ * storage mode (a training loop: the reference's gradient<float> called with new
+ * theta and psi0 every step, bench.cpp:114-133); the host psi0 is staged through
+ * a pinned buffer by host threads, overlapped with the DMA. Creating a plan on
+ * the context drops the cached one first. enable = 0 turns the cache off and
+ * frees the cached plan and the staging buffer. Default on. */
+int qf_ctx_set_plan_cache(qf_ctx *ctx, int enable);
 
 /* One-shot fused forward + adjoint gradient (the reference's
  * gradient<float> / run_checkpointed<float>). layers: number of equal
@@ -119,6 +127,14 @@ int qf_gradient_pergate_c64(qf_ctx *ctx, const qf_gate *gates, size_t n_gates,
                             const double *theta, uint64_t x_mask, uint64_t z_mask,
                             double *loss_out, double *grad_out, double *expect_out,
                             qf_stats *stats_out);
+
+/* Forward only (the reference's forward<float>, engine.hpp:131-133): the final
+ * state psi_M before the observable, batch*2^(n+1) floats to host, global phase
+ * included (amplitude for amplitude the reference's). One-shot like
+ * qf_gradient_c64 (plan cached in the context). */
+int qf_forward_c64(qf_ctx *ctx, const qf_gate *gates, size_t n_gates, uint32_t n_qubits,
+                   uint32_t n_params, uint32_t layers, const float *psi0, uint32_t batch,
+                   const double *theta, float *psi_out, qf_stats *stats_out);
 
 /* complex128 (the reference's double instantiations, engine.cpp:942,
  * checkpoint.cpp:196-213): psi0 is batch*2^(n+1) doubles. Fused fp64 segments:
@@ -155,7 +171,13 @@ int qf_plan_create_ex(qf_ctx *ctx, const qf_gate *gates, size_t n_gates, uint32_
 int qf_plan_destroy(qf_plan *plan);
 /* Batch store input. Host (pageable or pinned) -> device copy. */
 int qf_plan_upload_psi0(qf_plan *plan, const float *psi0_host);
-/* Or point the plan at caller-owned device memory (not copied, not modified). */
+/* Or point the plan at caller-owned device memory (batch*2^(n+1) floats on the
+ * plan's device, 16-byte aligned; batch*2^n a multiple of 16): it is aliased,
+ * not copied and never written, and stays bound until the next
+ * qf_plan_upload_psi0 / qf_plan_random_psi0 (which go back to the plan's own
+ * store). Every later gradient reads it on the plan's stream (qf_plan_stream):
+ * the caller orders its writes to the buffer before those calls (same stream,
+ * or an event the plan stream waits on) and keeps it alive while bound. */
 int qf_plan_set_psi0_device(qf_plan *plan, const float *psi0_device);
 /* Fused forward + adjoint gradient. theta/outputs are HOST pointers. */
 int qf_plan_gradient(qf_plan *plan, const double *theta, double *loss_out, double *grad_out,

@@ -22,7 +22,9 @@ QF_OK, QF_EINVAL, QF_ECAPACITY, QF_EDEVICE = 0, 2, 3, 4
 # exported symbols, in include/qfuse_b200.h order
 SYMBOLS = (
     "qf_last_error", "qf_version", "qf_ctx_create", "qf_ctx_destroy", "qf_ctx_set_hbm_limit",
-    "qf_gradient_c64", "qf_gradient_c64_ex", "qf_gradient_pergate_c64", "qf_gradient_c128",
+    "qf_ctx_set_plan_cache",
+    "qf_gradient_c64", "qf_gradient_c64_ex", "qf_gradient_pergate_c64", "qf_forward_c64",
+    "qf_gradient_c128",
     "qf_gradient_pergate_c128",
     "qf_plan_create",
     "qf_plan_create_ex", "qf_plan_destroy",
@@ -92,12 +94,15 @@ def load(path: str = LIB_PATH):
     L.qf_ctx_create.argtypes = [C.c_int, C.POINTER(_P)]
     L.qf_ctx_destroy.argtypes = [_P]
     L.qf_ctx_set_hbm_limit.argtypes = [_P, C.c_uint64]
+    L.qf_ctx_set_plan_cache.argtypes = [_P, C.c_int]
     grad_args = [_P, _P, C.c_size_t, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, _P,
                  C.c_uint32, _P, C.c_uint64, C.c_uint64, C.POINTER(C.c_double), _P, _P,
                  C.POINTER(QfStats)]
     L.qf_gradient_c64.argtypes = grad_args
     L.qf_gradient_pergate_c64.argtypes = grad_args
     L.qf_gradient_c64_ex.argtypes = grad_args[:7] + [C.c_uint32] + grad_args[7:]
+    L.qf_forward_c64.argtypes = [_P, _P, C.c_size_t, C.c_uint32, C.c_uint32, C.c_uint32, _P,
+                                 C.c_uint32, _P, _P, C.POINTER(QfStats)]
     L.qf_gradient_c128.argtypes = grad_args
     L.qf_gradient_pergate_c128.argtypes = grad_args
     L.qf_plan_create.argtypes = [_P, _P, C.c_size_t, C.c_uint32, C.c_uint32, C.c_uint32,
@@ -151,6 +156,24 @@ def _ptr(a):
     return None if a is None else a.ctypes.data_as(C.c_void_p)
 
 
+def _psi0_batch(a, n_qubits: int) -> int:
+    """Batch size of a psi0 array ((batch, 2^n, 2) or flat batch*2^(n+1)); the C
+    side reads exactly batch * 2^(n+1) values, so a mismatch is rejected here."""
+    per = 2 << n_qubits
+    batch = a.shape[0] if a.ndim >= 2 else a.size // per
+    if batch <= 0 or a.size != batch * per:
+        raise QfInvalidArgument(QF_EINVAL, f"psi0 has {a.size} values, not batch * 2^(n+1) "
+                                           f"for n = {n_qubits}")
+    return batch
+
+
+def _theta(theta, n_params: int):
+    th = np.ascontiguousarray(theta, np.float64)
+    if th.size != n_params:
+        raise QfInvalidArgument(QF_EINVAL, "gradient: theta length mismatch")
+    return th
+
+
 def _gates(gates):
     g = np.ascontiguousarray(gates)
     if g.dtype != GATE_DTYPE:
@@ -168,6 +191,10 @@ class Context:
 
     def set_hbm_limit(self, nbytes: int):
         _check(_lib.qf_ctx_set_hbm_limit(self.h, nbytes))
+
+    def set_plan_cache(self, enable: bool):
+        """One-shot calls reuse their plan while the circuit/shape repeats (default on)."""
+        _check(_lib.qf_ctx_set_plan_cache(self.h, 1 if enable else 0))
 
     def close(self):
         if self.h:
@@ -285,8 +312,8 @@ def gradient_c64(ctx: Context, gates, n_qubits, n_params, layers, ckpt_layers, p
     storage "memsave" = StorageMode::MemSave (qf_gradient_c64_ex)."""
     g = _gates(gates)
     a = np.ascontiguousarray(psi0, np.float32)
-    batch = a.shape[0]
-    th = np.ascontiguousarray(theta, np.float64)
+    batch = _psi0_batch(a, n_qubits)
+    th = _theta(theta, n_params)
     grad = np.empty(n_params, np.float64)
     exp = np.empty(batch, np.float64)
     loss = C.c_double()
@@ -304,14 +331,28 @@ def gradient_c64(ctx: Context, gates, n_qubits, n_params, layers, ckpt_layers, p
     return GradientResult(loss.value, grad, exp, st.as_dict())
 
 
+def forward_c64(ctx: Context, gates, n_qubits, n_params, layers, psi0, theta) -> np.ndarray:
+    """One-shot qf_forward_c64 (the reference's forward<float>): final state
+    (batch, 2^n, 2) float32, global phase included."""
+    g = _gates(gates)
+    a = np.ascontiguousarray(psi0, np.float32)
+    batch = _psi0_batch(a, n_qubits)
+    th = _theta(theta, n_params)
+    out = np.empty((batch, 1 << n_qubits, 2), np.float32)
+    st = QfStats()
+    _check(_lib.qf_forward_c64(ctx.h, _ptr(g), len(g), n_qubits, n_params, layers, _ptr(a), batch,
+                               _ptr(th), _ptr(out), C.byref(st)))
+    return out
+
+
 def gradient_c128(ctx: Context, gates, n_qubits, n_params, layers, ckpt_layers, psi0, theta,
                   pauli, pergate: bool = False) -> GradientResult:
     """qf_gradient_c128: the reference's gradient<double> (complex128 state, fp64 compute,
     fused segments); pergate=True: qf_gradient_pergate_c128 (naive_gradient<double>)."""
     g = _gates(gates)
     a = np.ascontiguousarray(psi0, np.float64)
-    batch = a.shape[0]
-    th = np.ascontiguousarray(theta, np.float64)
+    batch = _psi0_batch(a, n_qubits)
+    th = _theta(theta, n_params)
     grad = np.empty(n_params, np.float64)
     exp = np.empty(batch, np.float64)
     loss = C.c_double()
@@ -406,8 +447,8 @@ def gradient_c64_multi(n_gpus: int, gates, n_qubits, n_params, layers, ckpt_laye
     load()
     g = _gates(gates)
     a = np.ascontiguousarray(psi0, np.float32)
-    batch = a.shape[0]
-    th = np.ascontiguousarray(theta, np.float64)
+    batch = _psi0_batch(a, n_qubits)
+    th = _theta(theta, n_params)
     grad = np.empty(n_params, np.float64)
     exp = np.empty(batch, np.float64)
     loss = C.c_double()

@@ -57,7 +57,7 @@ def new_random_state(n_qubits: int, batch: int, seed: int, dtype=np.float32) -> 
         r = np.sqrt(-2.0 * np.log(u1))
         t = 2.0 * 3.14159265358979323846 * u2
         re, im = r * np.cos(t), r * np.sin(t)
-        inv = 1.0 / np.sqrt(np.sum(re * re + im * im))
+        inv = 1.0 / np.sqrt(np.cumsum(re * re + im * im)[-1])  # sequential, statevec.cpp:40-46
         out[s, :, 0] = re * inv
         out[s, :, 1] = im * inv
     return out

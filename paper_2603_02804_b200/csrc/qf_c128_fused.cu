@@ -498,9 +498,12 @@ cudaError_t launch_c128_segment(cudaStream_t st, bool backward, int grid, const 
     const size_t amps = size_t(1) << sg.m;
     if (backward) {
         const size_t smem = amps * 4 * sizeof(double2) + size_t(kC128MaxSec) * 64 * sizeof(double);
-        static const cudaError_t attr = cudaFuncSetAttribute(
-            seg_c128<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-            int((size_t(4) << kC128TileBits) * sizeof(double2) + size_t(kC128MaxSec) * 64 * sizeof(double)));
+        static std::atomic<uint64_t> done{0};
+        const cudaError_t attr = once_per_device(done, [] {
+            return cudaFuncSetAttribute(
+                seg_c128<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                int((size_t(4) << kC128TileBits) * sizeof(double2) + size_t(kC128MaxSec) * 64 * sizeof(double)));
+        });
         if (attr != cudaSuccess) return attr;
         seg_c128<true><<<grid, kT, smem, st>>>(sg, ops, cz, secU, psi, lam, n, tiles, kpart, ticket, K);
     } else {

@@ -17,6 +17,7 @@
 #include <memory>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/qfuse_b200.h"
@@ -141,6 +142,18 @@ struct qf_ctx {
     int sms = 148;
     uint64_t hbm_limit = 0;
     cudaStream_t stream = nullptr;
+    // One-shot entry points (qf_gradient_c64*, the reference-signature calls): the
+    // last plan is kept and reused while the next call has the same circuit, shape
+    // and storage mode (a training loop calls gradient<float> with new theta and
+    // psi0 every step, bench.cpp:114-133), so a call costs its H2D + the gradient,
+    // not a plan build. Explicit plan creation on the context drops it first.
+    qf_plan *cached = nullptr;
+    std::string cache_key;
+    bool cache_enabled = true;
+    // pinned staging of host psi0 for the one-shot calls (filled by host threads,
+    // DMA'd chunk by chunk while the next chunks are still being copied)
+    float *stage = nullptr;
+    size_t stage_bytes = 0;
 };
 
 struct qf_plan {
@@ -150,8 +163,10 @@ struct qf_plan {
     uint64_t amps = 0;        // B * 2^n
     uint64_t amps_padded = 0; // multiple of one tile
     size_t state_bytes = 0;
-    // stores
+    // stores. psi0 is the plan's own input buffer; psi0_src is where the passes read
+    // psi0 from (psi0, or caller memory bound by qf_plan_set_psi0_device)
     float2 *psi0 = nullptr, *W = nullptr, *lam = nullptr, *slots = nullptr;
+    const float2 *psi0_src = nullptr;
     // StorageMode::MemSave (streaming plans): checkpoint slots as bfloat16 pairs,
     // the final state stays complex64 in W
     uint32_t storage = QF_STORAGE_FULL;
@@ -162,7 +177,7 @@ struct qf_plan {
     double *theta = nullptr, *out = nullptr;
     float2 *ry = nullptr;
     DiagTab *dtab = nullptr;
-    double *wg = nullptr, *wa = nullptr, *wfinal = nullptr, *sec_gamma = nullptr;
+    double *wg = nullptr, *wa = nullptr, *wfinal = nullptr, *sec_gamma = nullptr, *sec_phase = nullptr;
     // theta-independent tables
     CzTab *cztab = nullptr;
     uint32_t *tileinfo = nullptr;
@@ -287,6 +302,7 @@ void build_device_plan(qf_plan *pl) {
 
     auto &o = pl->owned;
     pl->psi0 = dalloc<float2>(pl->amps_padded, o);
+    pl->psi0_src = pl->psi0;
     ck(cudaMemset(pl->psi0, 0, pl->state_bytes), "memset");
     pl->lam = dalloc<float2>(pl->amps_padded, o);
     if (!P.resident) pl->W = dalloc<float2>(pl->amps_padded, o);
@@ -305,9 +321,11 @@ void build_device_plan(qf_plan *pl) {
     pl->wa = dalloc<double>(size_t(S + 1) * n, o);
     ck(cudaMemset(pl->wg, 0, size_t(S + 1) * n * 8), "memset");
     ck(cudaMemset(pl->wa, 0, size_t(S + 1) * n * 8), "memset");
-    pl->wfinal = dalloc<double>(n, o);
+    pl->wfinal = dalloc<double>(n + 1, o); // [n]: global phase (forward-state readout)
+    ck(cudaMemset(pl->wfinal, 0, (n + 1) * sizeof(double)), "memset");
     pl->dtab = dalloc<DiagTab>(std::max<uint32_t>(S, 1), o);
     pl->sec_gamma = dalloc<double>(P.sec_q.size(), o);
+    pl->sec_phase = dalloc<double>(P.sec_q.size(), o);
     pl->cztab = dupload(P.cztab, o);
     std::vector<uint32_t> ti_all;
     for (const auto &t : P.tileinfo) {
@@ -335,6 +353,7 @@ void build_device_plan(qf_plan *pl) {
     if (P.resident) {
         const uint64_t rows = pl->amps_padded / 16;
         pl->r_psi0 = flat_map(pl->psi0, rows, 1, pl->state_bytes);
+        // (bind_psi0 re-encodes r_psi0 / m_psi0 for caller memory)
         pl->r_slots = flat_map(pl->slots, rows, std::max<uint32_t>(1, P.n_slots), pl->state_bytes);
         pl->r_out = flat_map(pl->lam, rows, 1, pl->state_bytes);
     } else {
@@ -362,6 +381,29 @@ void build_device_plan(qf_plan *pl) {
     ck(cudaDeviceSynchronize(), "plan setup");
 }
 
+// Points the passes' psi0 maps at `src` (the plan's own buffer or caller memory
+// of batch * 2^n complex64). TMA reads rows of 128 B: caller memory must be
+// 16-B aligned and cover whole rows (batch * 2^n a multiple of 16 amplitudes).
+void bind_psi0(qf_plan *pl, const float2 *src) {
+    if (src == pl->psi0_src) return;
+    const Plan &P = pl->P;
+    if (src != pl->psi0) {
+        if (reinterpret_cast<uintptr_t>(src) & 15u)
+            throw std::invalid_argument("qf_plan_set_psi0_device: pointer must be 16-byte aligned");
+        if (pl->amps % 16u)
+            throw std::invalid_argument("qf_plan_set_psi0_device: batch * 2^n must be a multiple of 16");
+    }
+    void *base = const_cast<float2 *>(src);
+    if (P.resident) {
+        // rows of the caller's buffer only; TMA fills the padded tail with zeros
+        const uint64_t rows = src == pl->psi0 ? pl->amps_padded / 16 : pl->amps / 16;
+        pl->r_psi0 = flat_map(base, rows, 1, pl->state_bytes);
+    } else {
+        for (size_t i = 0; i < P.layouts.size(); ++i) pl->m_psi0[i] = pass_map(base, P.layouts[i], P.n, P.batch);
+    }
+    pl->psi0_src = src;
+}
+
 // ---- the fused gradient, enqueued on the context stream
 void enqueue_prep(qf_plan *pl, const double *theta_dev, qf_stats &st) {
     const Plan &P = pl->P;
@@ -369,7 +411,7 @@ void enqueue_prep(qf_plan *pl, const double *theta_dev, qf_stats &st) {
     pl->timed(4, 0, [&] {
         ck(launch_prep_sections(s, int(P.sec_q.size()), pl->sec_q, pl->sec_stage, pl->sec_alpha,
                                 pl->sec_off, pl->sec_gates, theta_dev, int(P.n), pl->ry, pl->wg,
-                                pl->wa, pl->sec_gamma),
+                                pl->wa, pl->sec_gamma, pl->sec_phase),
            "prep_sections");
         ck(launch_diag_tables(s, int(P.stages), int(P.n), pl->wg, pl->wa, pl->stage_layout, pl->dq,
                               pl->dtab, pl->wfinal),
@@ -419,6 +461,8 @@ void enqueue_fused(qf_plan *pl, const double *theta_dev, double *out_dev, qf_sta
     cudaStream_t s = pl->ctx->stream;
     const uint32_t S = P.stages, n = P.n;
     enqueue_prep(pl, theta_dev, st);
+    if (forward_only)
+        ck(launch_phase_sum(s, int(P.sec_q.size()), pl->sec_phase, int(n), pl->wfinal), "phase sum");
     const double sb = double(pl->amps) * 8.0; // algorithmic bytes of one state
     double bytes = 0.0;
     if (P.resident) {
@@ -457,7 +501,7 @@ void enqueue_fused(qf_plan *pl, const double *theta_dev, double *out_dev, qf_sta
     } else {
         const size_t NPS = P.steps.size();
         const bool ms = pl->memsave();
-        const float2 *final_state = !NPS ? pl->psi0
+        const float2 *final_state = !NPS ? pl->psi0_src
                                     : ms  ? pl->W
                                           : pl->slots + size_t(P.n_slots - 1) * pl->amps_padded;
         auto slot16 = [&](size_t pi) { return pl->slots16 + size_t(pi / P.ckpt_passes) * pl->amps_padded; };
@@ -559,7 +603,7 @@ void enqueue_pergate(qf_plan *pl, const double *theta_dev, double *out_dev, qf_s
     const double sb = double(pl->amps) * 8.0;
     double bytes = 0;
     float2 *psi = P.resident ? pl->slots : pl->W;
-    ck(cudaMemcpyAsync(psi, pl->psi0, pl->state_bytes, cudaMemcpyDeviceToDevice, s), "copy");
+    ck(cudaMemcpyAsync(psi, pl->psi0_src, pl->amps * 8, cudaMemcpyDeviceToDevice, s), "copy");
     for (const qf_gate &g : P.gates) {
         pl->timed(5, 2 * sb, [&] {
             ck(launch_gate_fwd(s, psi, int(n), P.batch, g.kind, g.axis, g.q0, g.q1, theta_dev, g.param), "gate fwd");
@@ -568,7 +612,7 @@ void enqueue_pergate(qf_plan *pl, const double *theta_dev, double *out_dev, qf_s
         st.forward_passes++;
         bytes += 2 * sb;
     }
-    ck(cudaMemsetAsync(pl->wfinal, 0, n * sizeof(double), s), "memset");
+    ck(cudaMemsetAsync(pl->wfinal, 0, (n + 1) * sizeof(double), s), "memset");
     SeedParams sp{};
     sp.n = int(n);
     sp.batch = P.batch;
@@ -612,6 +656,12 @@ void enqueue_pergate(qf_plan *pl, const double *theta_dev, double *out_dev, qf_s
     st.passes_per_layer = P.layers ? uint32_t(P.gates.size() / P.layers) : 0;
 }
 
+void drop_cache(qf_ctx *ctx) {
+    delete ctx->cached;
+    ctx->cached = nullptr;
+    ctx->cache_key.clear();
+}
+
 qf_plan *create_plan(qf_ctx *ctx, const qf_gate *gates, size_t n_gates, uint32_t n, uint32_t n_params,
                      uint32_t layers, uint32_t ckpt, uint32_t batch, uint64_t x, uint64_t z,
                      uint32_t storage = QF_STORAGE_FULL) {
@@ -622,8 +672,95 @@ qf_plan *create_plan(qf_ctx *ctx, const qf_gate *gates, size_t n_gates, uint32_t
     pl->ctx = ctx;
     pl->storage = storage;
     pl->P = make_plan(gates, n_gates, n, n_params, layers, ckpt, batch, x, z);
+    drop_cache(ctx); // the one-shot cache must not hold HBM a new plan needs
     build_device_plan(pl.get());
     return pl.release();
+}
+
+// Plan of a one-shot call: the context's cached plan when the call has the same
+// gates, shape and storage mode as the last one, else a new plan (which then
+// replaces the cache). `owned` is set when the caller must free it (cache off).
+qf_plan *oneshot_plan(qf_ctx *ctx, const qf_gate *gates, size_t n_gates, uint32_t n, uint32_t n_params,
+                      uint32_t layers, uint32_t ckpt, uint32_t batch, uint64_t x, uint64_t z,
+                      uint32_t storage, bool &owned) {
+    if (!ctx) throw std::invalid_argument("null context");
+    if (n_gates && !gates) throw std::invalid_argument("null gate list");
+    std::string key(sizeof(uint32_t) * 6 + sizeof(uint64_t) * 2 + n_gates * sizeof(qf_gate), '\0');
+    char *k = key.data();
+    const uint32_t head[6] = {n, n_params, layers, ckpt, batch, storage};
+    const uint64_t masks[2] = {x, z};
+    std::memcpy(k, head, sizeof(head));
+    std::memcpy(k + sizeof(head), masks, sizeof(masks));
+    if (n_gates) std::memcpy(k + sizeof(head) + sizeof(masks), gates, n_gates * sizeof(qf_gate));
+    owned = false;
+    if (ctx->cache_enabled && ctx->cached && ctx->cache_key == key) return ctx->cached;
+    qf_plan *pl = create_plan(ctx, gates, n_gates, n, n_params, layers, ckpt, batch, x, z, storage);
+    if (ctx->cache_enabled) {
+        ctx->cached = pl;
+        ctx->cache_key = std::move(key);
+    } else {
+        owned = true;
+    }
+    return pl;
+}
+
+// Host psi0 (pageable, the caller's BatchedState storage) -> the plan's psi0 through
+// the context's pinned staging buffer: host threads copy 16 MiB chunks while the
+// chunks already staged are DMA'd in order (copy and transfer overlap). Pinned
+// sources and small states go straight to cudaMemcpyAsync.
+void stage_psi0(qf_plan *pl, const float *src) {
+    qf_ctx *c = pl->ctx;
+    const size_t bytes = size_t(pl->amps) * 8;
+    bind_psi0(pl, pl->psi0);
+    cudaPointerAttributes attr{};
+    const bool pinned = cudaPointerGetAttributes(&attr, src) == cudaSuccess && attr.type == cudaMemoryTypeHost;
+    cudaGetLastError();
+    if (pinned || bytes < (size_t(8) << 20)) {
+        ck(cudaMemcpyAsync(pl->psi0, src, bytes, cudaMemcpyHostToDevice, c->stream), "H2D psi0");
+        return;
+    }
+    ck(cudaStreamSynchronize(c->stream), "staging"); // no DMA still reads the staging buffer
+    if (c->stage_bytes < bytes) {
+        if (c->stage) cudaFreeHost(c->stage);
+        c->stage = nullptr;
+        c->stage_bytes = 0;
+        void *h = nullptr;
+        if (cudaMallocHost(&h, bytes) != cudaSuccess) {
+            cudaGetLastError();
+            throw CapacityError("pinned staging buffer of " + std::to_string(bytes >> 20) + " MiB failed");
+        }
+        c->stage = static_cast<float *>(h);
+        c->stage_bytes = bytes;
+    }
+    constexpr size_t kChunk = size_t(16) << 20;
+    const size_t nchunks = (bytes + kChunk - 1) / kChunk;
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    const size_t T = std::min<size_t>({size_t(8), size_t(hw), nchunks});
+    std::unique_ptr<std::atomic<int>[]> ready(new std::atomic<int>[nchunks]);
+    for (size_t i = 0; i < nchunks; ++i) ready[i].store(0, std::memory_order_relaxed);
+    char *dst = reinterpret_cast<char *>(c->stage);
+    const char *from = reinterpret_cast<const char *>(src);
+    auto work = [&](size_t t) {
+        for (size_t i = t; i < nchunks; i += T) {
+            const size_t off = i * kChunk, len = std::min(kChunk, bytes - off);
+            std::memcpy(dst + off, from + off, len);
+            ready[i].store(1, std::memory_order_release);
+        }
+    };
+    struct Joiner {
+        std::vector<std::thread> v;
+        ~Joiner() {
+            for (auto &t : v)
+                if (t.joinable()) t.join();
+        }
+    } threads;
+    for (size_t t = 0; t < T; ++t) threads.v.emplace_back(work, t);
+    char *ddst = reinterpret_cast<char *>(pl->psi0);
+    for (size_t i = 0; i < nchunks; ++i) {
+        while (!ready[i].load(std::memory_order_acquire)) std::this_thread::yield();
+        const size_t off = i * kChunk, len = std::min(kChunk, bytes - off);
+        ck(cudaMemcpyAsync(ddst + off, dst + off, len, cudaMemcpyHostToDevice, c->stream), "H2D psi0");
+    }
 }
 
 enum class Mode { Fused, PerGate };
@@ -826,6 +963,8 @@ int qf_ctx_destroy(qf_ctx *ctx) {
     return guarded([&] {
         if (!ctx) return;
         cudaSetDevice(ctx->device);
+        drop_cache(ctx);
+        if (ctx->stage) cudaFreeHost(ctx->stage);
         if (ctx->stream) cudaStreamDestroy(ctx->stream);
         delete ctx;
     });
@@ -835,6 +974,20 @@ int qf_ctx_set_hbm_limit(qf_ctx *ctx, uint64_t bytes) {
     return guarded([&] {
         if (!ctx) throw std::invalid_argument("null context");
         ctx->hbm_limit = bytes;
+    });
+}
+
+int qf_ctx_set_plan_cache(qf_ctx *ctx, int enable) {
+    return guarded([&] {
+        if (!ctx) throw std::invalid_argument("null context");
+        ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+        ctx->cache_enabled = enable != 0;
+        if (!enable) {
+            drop_cache(ctx);
+            if (ctx->stage) cudaFreeHost(ctx->stage);
+            ctx->stage = nullptr;
+            ctx->stage_bytes = 0;
+        }
     });
 }
 
@@ -866,6 +1019,7 @@ int qf_plan_upload_psi0(qf_plan *plan, const float *psi0_host) {
     return guarded([&] {
         if (!plan || !psi0_host) throw std::invalid_argument("null argument");
         ck(cudaSetDevice(plan->ctx->device), "cudaSetDevice");
+        bind_psi0(plan, plan->psi0);
         ck(cudaMemcpyAsync(plan->psi0, psi0_host, plan->amps * 8, cudaMemcpyHostToDevice,
                            plan->ctx->stream),
            "H2D psi0");
@@ -876,9 +1030,7 @@ int qf_plan_set_psi0_device(qf_plan *plan, const float *psi0_device) {
     return guarded([&] {
         if (!plan || !psi0_device) throw std::invalid_argument("null argument");
         ck(cudaSetDevice(plan->ctx->device), "cudaSetDevice");
-        ck(cudaMemcpyAsync(plan->psi0, psi0_device, plan->amps * 8, cudaMemcpyDeviceToDevice,
-                           plan->ctx->stream),
-           "D2D psi0");
+        bind_psi0(plan, reinterpret_cast<const float2 *>(psi0_device)); // aliased, not copied
     });
 }
 
@@ -910,22 +1062,48 @@ int qf_plan_gradient_device(qf_plan *plan, const double *theta_dev, double *out_
     });
 }
 
+namespace {
+// Forward-only readout of `plan` with host theta: the final state before the
+// observable (global phase restored), complex64 to host.
+void forward_state(qf_plan *plan, const double *theta, float *psi_out_host) {
+    ck(cudaSetDevice(plan->ctx->device), "cudaSetDevice");
+    const Plan &P = plan->P;
+    cudaStream_t s = plan->ctx->stream;
+    if (P.n_params) {
+        if (!theta) throw std::invalid_argument("forward: theta length mismatch");
+        std::memcpy(plan->h_theta, theta, sizeof(double) * P.n_params);
+        ck(cudaMemcpyAsync(plan->theta, plan->h_theta, sizeof(double) * P.n_params,
+                           cudaMemcpyHostToDevice, s),
+           "H2D");
+    }
+    qf_stats st{};
+    enqueue_fused(plan, plan->theta, plan->out, st, /*forward_only=*/true);
+    ck(cudaMemcpyAsync(psi_out_host, plan->lam, plan->amps * 8, cudaMemcpyDeviceToHost, s), "D2H");
+    ck(cudaStreamSynchronize(s), "forward");
+    plan->last = st;
+}
+} // namespace
+
 int qf_plan_forward_state(qf_plan *plan, const double *theta, float *psi_out_host) {
     return guarded([&] {
         if (!plan || !psi_out_host) throw std::invalid_argument("null argument");
-        ck(cudaSetDevice(plan->ctx->device), "cudaSetDevice");
-        const Plan &P = plan->P;
-        cudaStream_t s = plan->ctx->stream;
-        if (P.n_params) {
-            std::memcpy(plan->h_theta, theta, sizeof(double) * P.n_params);
-            ck(cudaMemcpyAsync(plan->theta, plan->h_theta, sizeof(double) * P.n_params,
-                               cudaMemcpyHostToDevice, s),
-               "H2D");
-        }
-        qf_stats st{};
-        enqueue_fused(plan, plan->theta, plan->out, st, /*forward_only=*/true);
-        ck(cudaMemcpyAsync(psi_out_host, plan->lam, plan->amps * 8, cudaMemcpyDeviceToHost, s), "D2H");
-        ck(cudaStreamSynchronize(s), "forward");
+        forward_state(plan, theta, psi_out_host);
+    });
+}
+
+int qf_forward_c64(qf_ctx *ctx, const qf_gate *gates, size_t n_gates, uint32_t n_qubits,
+                   uint32_t n_params, uint32_t layers, const float *psi0, uint32_t batch,
+                   const double *theta, float *psi_out, qf_stats *stats_out) {
+    return guarded([&] {
+        if (!psi0 || !psi_out) throw std::invalid_argument("null argument");
+        bool owned = false;
+        qf_plan *pl = oneshot_plan(ctx, gates, n_gates, n_qubits, n_params, layers, 0, batch, 0, 0,
+                                   QF_STORAGE_FULL, owned);
+        std::unique_ptr<qf_plan> own(owned ? pl : nullptr);
+        ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+        stage_psi0(pl, psi0);
+        forward_state(pl, theta, psi_out);
+        if (stats_out) *stats_out = pl->last;
     });
 }
 
@@ -955,10 +1133,13 @@ int qf_gradient_c64(qf_ctx *ctx, const qf_gate *gates, size_t n_gates, uint32_t 
                     double *loss_out, double *grad_out, double *expect_out, qf_stats *stats_out) {
     return guarded([&] {
         if (!psi0) throw std::invalid_argument("null psi0");
-        std::unique_ptr<qf_plan> pl(create_plan(ctx, gates, n_gates, n_qubits, n_params, layers,
-                                                ckpt_layers, batch, x_mask, z_mask));
-        ck(cudaMemcpyAsync(pl->psi0, psi0, pl->amps * 8, cudaMemcpyHostToDevice, ctx->stream), "H2D psi0");
-        run_host(pl.get(), theta, loss_out, grad_out, expect_out, stats_out, Mode::Fused);
+        bool owned = false;
+        qf_plan *pl = oneshot_plan(ctx, gates, n_gates, n_qubits, n_params, layers, ckpt_layers, batch,
+                                   x_mask, z_mask, QF_STORAGE_FULL, owned);
+        std::unique_ptr<qf_plan> own(owned ? pl : nullptr);
+        ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+        stage_psi0(pl, psi0);
+        run_host(pl, theta, loss_out, grad_out, expect_out, stats_out, Mode::Fused);
     });
 }
 
@@ -969,10 +1150,13 @@ int qf_gradient_c64_ex(qf_ctx *ctx, const qf_gate *gates, size_t n_gates, uint32
                        double *grad_out, double *expect_out, qf_stats *stats_out) {
     return guarded([&] {
         if (!psi0) throw std::invalid_argument("null psi0");
-        std::unique_ptr<qf_plan> pl(create_plan(ctx, gates, n_gates, n_qubits, n_params, layers,
-                                                ckpt_layers, batch, x_mask, z_mask, storage_mode));
-        ck(cudaMemcpyAsync(pl->psi0, psi0, pl->amps * 8, cudaMemcpyHostToDevice, ctx->stream), "H2D psi0");
-        run_host(pl.get(), theta, loss_out, grad_out, expect_out, stats_out, Mode::Fused);
+        bool owned = false;
+        qf_plan *pl = oneshot_plan(ctx, gates, n_gates, n_qubits, n_params, layers, ckpt_layers, batch,
+                                   x_mask, z_mask, storage_mode, owned);
+        std::unique_ptr<qf_plan> own(owned ? pl : nullptr);
+        ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+        stage_psi0(pl, psi0);
+        run_host(pl, theta, loss_out, grad_out, expect_out, stats_out, Mode::Fused);
     });
 }
 
@@ -983,10 +1167,13 @@ int qf_gradient_pergate_c64(qf_ctx *ctx, const qf_gate *gates, size_t n_gates, u
                             double *expect_out, qf_stats *stats_out) {
     return guarded([&] {
         if (!psi0) throw std::invalid_argument("null psi0");
-        std::unique_ptr<qf_plan> pl(create_plan(ctx, gates, n_gates, n_qubits, n_params, layers,
-                                                ckpt_layers, batch, x_mask, z_mask));
-        ck(cudaMemcpyAsync(pl->psi0, psi0, pl->amps * 8, cudaMemcpyHostToDevice, ctx->stream), "H2D psi0");
-        run_host(pl.get(), theta, loss_out, grad_out, expect_out, stats_out, Mode::PerGate);
+        bool owned = false;
+        qf_plan *pl = oneshot_plan(ctx, gates, n_gates, n_qubits, n_params, layers, ckpt_layers, batch,
+                                   x_mask, z_mask, QF_STORAGE_FULL, owned);
+        std::unique_ptr<qf_plan> own(owned ? pl : nullptr);
+        ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+        stage_psi0(pl, psi0);
+        run_host(pl, theta, loss_out, grad_out, expect_out, stats_out, Mode::PerGate);
     });
 }
 
@@ -1065,7 +1252,7 @@ extern "C" int qf_plan_download_psi0(qf_plan *plan, float *psi0_host) {
     return guarded([&] {
         if (!plan || !psi0_host) throw std::invalid_argument("null argument");
         ck(cudaSetDevice(plan->ctx->device), "cudaSetDevice");
-        ck(cudaMemcpyAsync(psi0_host, plan->psi0, plan->amps * 8, cudaMemcpyDeviceToHost,
+        ck(cudaMemcpyAsync(psi0_host, plan->psi0_src, plan->amps * 8, cudaMemcpyDeviceToHost,
                            plan->ctx->stream),
            "D2H psi0");
         ck(cudaStreamSynchronize(plan->ctx->stream), "D2H psi0");

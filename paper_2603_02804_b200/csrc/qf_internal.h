@@ -3,6 +3,7 @@
 // qf_pergate.cu). Not part of the C-ABI.
 #pragma once
 
+#include <atomic>
 #include <cstddef>
 #include <cstdint>
 #include <vector>
@@ -149,7 +150,11 @@ cudaError_t launch_prep_sections(cudaStream_t st, int n_sec, const uint32_t *sec
                                  const uint32_t *sec_stage, const uint32_t *sec_alpha_row,
                                  const uint32_t *sec_off, const uint32_t *sec_gates,
                                  const double *theta, int n, float2 *ry, double *wg,
-                                 double *wa, double *sec_gamma);
+                                 double *wa, double *sec_gamma, double *sec_phase);
+// Forward-state readout: wfinal[n] = the global phase e^{i sum delta} the stage
+// model drops (it cancels in <O> and every gradient, not in the state itself).
+cudaError_t launch_phase_sum(cudaStream_t st, int n_sec, const double *sec_phase, int n,
+                             double *wfinal);
 // dq: [layouts][28] qubit of (reg 0..3, thr 0..7, tile 0..15), -1 = none.
 cudaError_t launch_diag_tables(cudaStream_t st, int stages, int n, const double *wg,
                                const double *wa, const int *stage_layout, const int *dq,
@@ -249,6 +254,21 @@ cudaError_t launch_c128_segment(cudaStream_t st, bool backward, int grid, const 
 cudaError_t launch_c128_finalize(cudaStream_t st, int nsec, const uint32_t *off, const uint32_t *cnt,
                                  const uint32_t *gates, const double *theta, const double *K,
                                  double *grad);
+
+// cudaFuncSetAttribute opt-ins (e.g. > 48 KiB of dynamic shared memory) are
+// per device: `set` runs once on every device the process launches on (bit d
+// of `done` = device d done). Racing first calls on one device both run `set`,
+// which is idempotent.
+template <class F> cudaError_t once_per_device(std::atomic<uint64_t> &done, F &&set) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const uint64_t bit = 1ull << (unsigned(dev) & 63u);
+    if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+    e = set();
+    if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_acq_rel);
+    return e;
+}
 
 // Sets the thread-local qf_last_error() text (qf_capi.cpp).
 void set_last_error(const char *msg);

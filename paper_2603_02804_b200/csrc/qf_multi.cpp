@@ -20,6 +20,7 @@
 #include <mutex>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/qfuse_b200.h"
@@ -105,6 +106,29 @@ void shard(uint32_t batch, int i, int g, uint32_t &start, uint32_t &count) {
     const uint32_t base = batch / uint32_t(g), extra = batch % uint32_t(g);
     start = uint32_t(i) * base + std::min<uint32_t>(uint32_t(i), extra);
     count = base + (uint32_t(i) < extra ? 1u : 0u);
+}
+
+// Runs f(0..G-1), f(i) on its own host thread for G > 1; the first failure
+// (QfFail / std::exception, with its qf_last_error text) is rethrown here.
+template <class F> void on_each_device(int G, F &&f) {
+    if (G == 1) {
+        f(0);
+        return;
+    }
+    std::vector<std::exception_ptr> err(G);
+    std::vector<std::thread> th;
+    th.reserve(G);
+    for (int i = 0; i < G; ++i)
+        th.emplace_back([&, i] {
+            try {
+                f(i);
+            } catch (...) {
+                err[i] = std::current_exception();
+            }
+        });
+    for (auto &t : th) t.join();
+    for (auto &e : err)
+        if (e) std::rethrow_exception(e);
 }
 
 } // namespace
@@ -233,8 +257,10 @@ void group_gradient(qf_group_plan *gp, const double *theta, double *loss, double
     const int G = int(gp->dev.size());
     const size_t M = gp->n_params, R = gp->red_len();
     if (M) std::memcpy(gp->h_theta, theta, sizeof(double) * M);
-    // 1) every device: theta H2D, the fused gradient of its shard into out
-    for (int i = 0; i < G; ++i) {
+    // 1) every device: theta H2D, the fused gradient of its shard into out. One
+    // host thread per device enqueues its ~10^2..10^3 launches, so all G devices
+    // start together instead of device i waiting for devices 0..i-1's enqueue.
+    auto enqueue = [&](int i) {
         qf_group_plan::Dev &d = gp->dev[i];
         cuda_ok(cudaSetDevice(g->devices[i]), "cudaSetDevice");
         cuda_ok(cudaEventRecord(d.ev0, d.stream), "event");
@@ -246,7 +272,8 @@ void group_gradient(qf_group_plan *gp, const double *theta, double *loss, double
             ok(qf_plan_gradient_device(d.plan, d.theta, d.out));
         else
             cuda_ok(cudaMemsetAsync(d.out, 0, sizeof(double) * R, d.stream), "memset");
-    }
+    };
+    on_each_device(G, enqueue);
     // 2) the single exchange: [grad | loss] summed over the group, in place
     api.check(api.group_start(), "ncclGroupStart");
     ncclResult_t rr = ncclSuccess;
@@ -339,10 +366,13 @@ int qf_group_plan_upload_psi0(qf_group_plan *gp, const float *psi0_host) {
     return guarded([&] {
         if (!gp || !psi0_host) throw QfFail(QF_EINVAL, "null argument");
         const size_t per = size_t(2) << gp->n; // floats per sample
-        for (auto &d : gp->dev)
-            if (d.plan) ok(qf_plan_upload_psi0(d.plan, psi0_host + per * d.start));
-        for (auto &d : gp->dev)
-            if (d.plan) ok(qf_plan_synchronize(d.plan));
+        on_each_device(int(gp->dev.size()), [&](int i) {
+            auto &d = gp->dev[i];
+            if (d.plan) {
+                ok(qf_plan_upload_psi0(d.plan, psi0_host + per * d.start));
+                ok(qf_plan_synchronize(d.plan));
+            }
+        });
     });
 }
 

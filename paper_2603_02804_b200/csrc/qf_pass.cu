@@ -374,26 +374,26 @@ int bwd_pipe() {
     return nb;
 }
 
-bool g_attrs = false;
+std::atomic<uint64_t> g_attrs{0};
 template <class K> cudaError_t set_smem(K kernel, size_t bytes) {
     return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
 }
 cudaError_t ensure_attrs() {
-    if (g_attrs) return cudaSuccess;
-    cudaError_t e = set_smem(pass_kernel<false, 2>, pass_smem(false, 2));
-    if (e == cudaSuccess) e = set_smem(pass_kernel<false, 2, kProgA>, pass_smem(false, 2));
-    if (e == cudaSuccess) e = set_smem(pass_kernel<false, 2, kProgB20>, pass_smem(false, 2));
-    if (e == cudaSuccess) e = set_smem(pass_kernel<false, 2, kProgB16>, pass_smem(false, 2));
-    if (e == cudaSuccess) e = set_smem(pass_kernel<false, 2, kProgB16x>, pass_smem(false, 2));
-    if (e == cudaSuccess) e = set_smem(pass_kernel<true, 1>, pass_smem(true, 1));
-    if (e == cudaSuccess) e = set_smem(pass_kernel<true, 3>, pass_smem(true, 3));
-    if (e == cudaSuccess) e = set_smem(pass_bwd_dual<0>, dual_smem());
-    if (e == cudaSuccess) e = set_smem(pass_bwd_dual<kProgA>, dual_smem());
-    if (e == cudaSuccess) e = set_smem(pass_bwd_dual<kProgB20>, dual_smem());
-    if (e == cudaSuccess) e = set_smem(pass_bwd_dual<kProgB16>, dual_smem());
-    if (e == cudaSuccess) e = set_smem(pass_bwd_dual<kProgB16x>, dual_smem());
-    g_attrs = e == cudaSuccess;
-    return e;
+    return once_per_device(g_attrs, [] {
+        cudaError_t e = set_smem(pass_kernel<false, 2>, pass_smem(false, 2));
+        if (e == cudaSuccess) e = set_smem(pass_kernel<false, 2, kProgA>, pass_smem(false, 2));
+        if (e == cudaSuccess) e = set_smem(pass_kernel<false, 2, kProgB20>, pass_smem(false, 2));
+        if (e == cudaSuccess) e = set_smem(pass_kernel<false, 2, kProgB16>, pass_smem(false, 2));
+        if (e == cudaSuccess) e = set_smem(pass_kernel<false, 2, kProgB16x>, pass_smem(false, 2));
+        if (e == cudaSuccess) e = set_smem(pass_kernel<true, 1>, pass_smem(true, 1));
+        if (e == cudaSuccess) e = set_smem(pass_kernel<true, 3>, pass_smem(true, 3));
+        if (e == cudaSuccess) e = set_smem(pass_bwd_dual<0>, dual_smem());
+        if (e == cudaSuccess) e = set_smem(pass_bwd_dual<kProgA>, dual_smem());
+        if (e == cudaSuccess) e = set_smem(pass_bwd_dual<kProgB20>, dual_smem());
+        if (e == cudaSuccess) e = set_smem(pass_bwd_dual<kProgB16>, dual_smem());
+        if (e == cudaSuccess) e = set_smem(pass_bwd_dual<kProgB16x>, dual_smem());
+        return e;
+    });
 }
 
 // QF_PROGS=0 forces the runtime-dispatch kernels (A/B timing).

@@ -57,7 +57,8 @@ __device__ inline M2 sec_gate(uint32_t enc, const double *theta, bool deriv) {
 __global__ void prep_sections_kernel(int n_sec, const uint32_t *sec_q, const uint32_t *sec_stage,
                                      const uint32_t *sec_alpha_row, const uint32_t *sec_off,
                                      const uint32_t *sec_gates, const double *theta, int n,
-                                     float2 *ry, double *wg, double *wa, double *sec_gamma) {
+                                     float2 *ry, double *wg, double *wa, double *sec_gamma,
+                                     double *sec_phase) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n_sec) return;
     M2 u{{1, 0}, {0, 0}, {0, 0}, {1, 0}};
@@ -89,6 +90,24 @@ __global__ void prep_sections_kernel(int n_sec, const uint32_t *sec_q, const uin
     wg[size_t(st) * n + q] = gamma;
     wa[size_t(sec_alpha_row[i]) * n + q] = alpha;
     sec_gamma[i] = gamma;
+    // global phase the device model drops: U = e^{i dth} Rz(a) Ry(b) Rz(g) and the
+    // diagonal tables apply Rz(w) as diag(1, e^{i w}) = e^{i w / 2} Rz(w)
+    sec_phase[i] = dth - 0.5 * (alpha + gamma);
+}
+
+// Forward-state readout only: wfinal[n] = sum of the sections' dropped phases
+// (fixed order: strided per-thread sums, then a sequential sum over threads).
+__global__ void phase_sum_kernel(int n_sec, const double *sec_phase, int n, double *wfinal) {
+    __shared__ double part[256];
+    double s = 0.0;
+    for (int i = threadIdx.x; i < n_sec; i += blockDim.x) s += sec_phase[i];
+    part[threadIdx.x] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int k = 0; k < int(blockDim.x); ++k) t += part[k];
+        wfinal[n] = t;
+    }
 }
 
 // Per stage: e^{i sum_q w_q x_q} tables of D_s in the layout of the pass that
@@ -252,10 +271,17 @@ cudaError_t launch_prep_sections(cudaStream_t st, int n_sec, const uint32_t *sec
                                  const uint32_t *sec_stage, const uint32_t *sec_alpha_row,
                                  const uint32_t *sec_off, const uint32_t *sec_gates,
                                  const double *theta, int n, float2 *ry, double *wg, double *wa,
-                                 double *sec_gamma) {
+                                 double *sec_gamma, double *sec_phase) {
     if (n_sec == 0) return cudaSuccess;
     prep_sections_kernel<<<(n_sec + 127) / 128, 128, 0, st>>>(
-        n_sec, sec_q, sec_stage, sec_alpha_row, sec_off, sec_gates, theta, n, ry, wg, wa, sec_gamma);
+        n_sec, sec_q, sec_stage, sec_alpha_row, sec_off, sec_gates, theta, n, ry, wg, wa, sec_gamma,
+        sec_phase);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_phase_sum(cudaStream_t st, int n_sec, const double *sec_phase, int n,
+                             double *wfinal) {
+    phase_sum_kernel<<<1, 256, 0, st>>>(n_sec, sec_phase, n, wfinal);
     return cudaGetLastError();
 }
 

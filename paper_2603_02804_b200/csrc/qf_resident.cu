@@ -54,8 +54,10 @@ __device__ __forceinline__ float2 seed_factor(uint32_t x, uint64_t X, uint64_t Z
     return make_float2(float(r2), float(i2));
 }
 // D_f(x) for the forward-state readout.
+// wf[n]: the global phase (launch_phase_sum), so the readout equals the reference's
+// forward<T> amplitude for amplitude (engine.hpp:131-133).
 __device__ __forceinline__ float2 dfinal(uint32_t x, int n, const double *wf, const CzAdj *czf) {
-    double ang = 0.0;
+    double ang = wf[n];
     for (int q = 0; q < n; ++q)
         if ((x >> q) & 1u) ang += wf[q];
     double s, c;
@@ -526,21 +528,22 @@ __global__ void __launch_bounds__(kThreads, 2)
     if (tid == 0) bulk_wait0();
 }
 
-bool g_attrs = false;
+std::atomic<uint64_t> g_attrs{0};
 
 } // namespace
 
 size_t resident_smem_bytes() { return res_smem(); }
 
 int resident_occupancy() {
-    if (!g_attrs) {
-        if (cudaFuncSetAttribute(resident_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 int(res_smem())) != cudaSuccess ||
-            cudaFuncSetAttribute(resident_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 int(res_smem())) != cudaSuccess)
-            return 0;
-        g_attrs = true;
-    }
+    const cudaError_t e = once_per_device(g_attrs, [] {
+        cudaError_t r = cudaFuncSetAttribute(resident_kernel<false>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, int(res_smem()));
+        if (r == cudaSuccess)
+            r = cudaFuncSetAttribute(resident_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(res_smem()));
+        return r;
+    });
+    if (e != cudaSuccess) return 0;
     int blocks = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, resident_kernel<false>, kThreads, res_smem());
     return blocks;

@@ -17,6 +17,7 @@ namespace qfuse::b200 {
 namespace {
 
 thread_local int t_device = -1;
+thread_local std::vector<int> t_devices; // > 1 entries: batch-sharded multi-GPU
 
 struct CtxDeleter {
     void operator()(qf_ctx *c) const { qf_ctx_destroy(c); }
@@ -82,10 +83,16 @@ GradientResult call(bool pergate, const std::vector<Gate> &flat, uint32_t n_qubi
                                       pauli.x_mask, pauli.z_mask, &r.loss, r.gradient.data(), nullptr, &st));
     } else {
         const uint32_t storage = mode == StorageMode::MemSave ? QF_STORAGE_MEMSAVE : QF_STORAGE_FULL;
-        check(qf_gradient_c64_ex(context(), gates.data(), gates.size(), n_qubits, n_params, layers,
-                                 block_layers, storage, psi0.components().data(), psi0.batch(),
-                                 theta.data(), pauli.x_mask, pauli.z_mask, &r.loss, r.gradient.data(),
-                                 nullptr, &st));
+        if (t_devices.size() > 1)
+            check(qf_gradient_c64_multi(int(t_devices.size()), t_devices.data(), gates.data(), gates.size(),
+                                        n_qubits, n_params, layers, block_layers, storage,
+                                        psi0.components().data(), psi0.batch(), theta.data(), pauli.x_mask,
+                                        pauli.z_mask, &r.loss, r.gradient.data(), nullptr, &st));
+        else
+            check(qf_gradient_c64_ex(context(), gates.data(), gates.size(), n_qubits, n_params, layers,
+                                     block_layers, storage, psi0.components().data(), psi0.batch(),
+                                     theta.data(), pauli.x_mask, pauli.z_mask, &r.loss, r.gradient.data(),
+                                     nullptr, &st));
     }
     r.stats.forward_traversals = st.forward_passes;
     r.stats.backward_traversals = st.backward_passes;
@@ -137,6 +144,29 @@ GradientResult call_c128(bool naive, const std::vector<Gate> &flat, uint32_t n_q
 } // namespace
 
 void set_device(int device) { t_device = device; }
+
+void set_devices(const std::vector<int> &devices) {
+    t_devices = devices;
+    if (devices.size() == 1) t_device = devices[0];
+}
+
+ForwardResult<float> forward(const FusedCircuit &fused, const BatchedState<float> &psi0,
+                             std::span<const double> theta, StorageMode, MemoryAccountant *accountant) {
+    if (theta.size() != fused.n_params)
+        throw std::invalid_argument("forward: theta length mismatch");
+    const auto gates = to_gates(flatten(fused));
+    ForwardResult<float> r{BatchedState<float>(psi0.n_qubits(), psi0.batch()), {}, {}};
+    qf_stats st{};
+    check(qf_forward_c64(context(), gates.data(), gates.size(), fused.n_qubits, fused.n_params, 0,
+                         psi0.components().data(), psi0.batch(), theta.data(),
+                         r.state.components().data(), &st));
+    r.stats.forward_traversals = st.forward_passes;
+    if (accountant != nullptr) { // the working store only
+        accountant->add(1.0);
+        accountant->release(1.0);
+    }
+    return r;
+}
 
 GradientResult gradient(const FusedCircuit &fused, const BatchedState<double> &psi0,
                         std::span<const double> theta, const PauliString &pauli,

@@ -19,6 +19,7 @@
 
 #include <cstdint>
 #include <span>
+#include <vector>
 
 #include "qfuse/checkpoint.hpp"
 #include "qfuse/circuit.hpp"
@@ -30,6 +31,19 @@ namespace qfuse::b200 {
 
 // CUDA device used by the calls of this thread (default 0, or $QFUSE_B200_DEVICE).
 void set_device(int device);
+// Batch-sharded multi-GPU for this thread's gradient / run_checkpointed calls
+// (complex64): the samples are split over `devices` in order and [grad | loss]
+// is summed with one NCCL all-reduce (qf_gradient_c64_multi). An
+// empty list (default) or one device = the single-device path. The per-gate
+// calls and complex128 stay on set_device's device.
+void set_devices(const std::vector<int> &devices);
+
+// forward<float> (engine.hpp:131-133): the final state before the observable,
+// amplitude for amplitude the reference's (global phase included). The ledger
+// of the result is empty: the device never stores per-op states.
+ForwardResult<float> forward(const FusedCircuit &fused, const BatchedState<float> &psi0,
+                             std::span<const double> theta, StorageMode mode,
+                             MemoryAccountant *accountant = nullptr);
 
 GradientResult gradient(const FusedCircuit &fused, const BatchedState<float> &psi0,
                         std::span<const double> theta, const PauliString &pauli,

@@ -46,6 +46,13 @@ class DataParallelGradient:
                 self.dist.all_reduce(self.out[: self.m + 1])
         return self.out
 
+    def close(self):
+        """Waits for this rank's queued work and drops the device buffers, so the
+        plan and its context (which own the stream) can be destroyed next."""
+        if self.out is not None:
+            self.stream.synchronize()
+            self.out = None
+
     def step_host(self, psi0_pinned, theta_host_pinned, theta_dev, result_host):
         """End-to-end step with host buffers: H2D psi0 + theta, gradient,
         all-reduce, D2H [grad | loss]. Returns result_host (pinned float64)."""

@@ -56,3 +56,27 @@ def test_group_api_without_device():
     assert lib.qf_group_destroy(None) == 0
     st = pkg.capi.QfStats()
     assert lib.qf_plan_last_stats(None, ctypes.byref(st)) == pkg.capi.QF_EINVAL
+
+
+def test_python_binding_validates_shapes():
+    """The one-shot wrappers check psi0 / theta sizes before the C side reads
+    batch * 2^(n+1) floats and n_params doubles from them (no device needed)."""
+    import numpy as np
+    import pytest
+    from paper_2603_02804_b200 import circuits as C
+    gates, npar = C.build_hea(4, 2)
+    pauli = C.parse_pauli("IXYZ")
+    theta = C.random_parameters(npar, 1)
+    flat = np.zeros(2 * 32 + 3, np.float32)  # not a whole number of 4-qubit samples
+    for fn in (pkg.capi.gradient_c64, pkg.capi.gradient_c64_multi):
+        args = (gates, 4, npar, 2, 0)
+        with pytest.raises(pkg.capi.QfInvalidArgument):
+            if fn is pkg.capi.gradient_c64:
+                fn(None, *args, flat, theta, pauli)
+            else:
+                fn(1, *args, flat, theta, pauli)
+    good = C.new_random_state(4, 2, 1)
+    with pytest.raises(pkg.capi.QfInvalidArgument):
+        pkg.capi.gradient_c64(None, gates, 4, npar, 2, 0, good, theta[:-1], pauli)
+    with pytest.raises(pkg.capi.QfInvalidArgument):
+        pkg.capi.gradient_c128(None, gates, 4, npar, 2, 0, good.astype(np.float64)[:, :5], theta, pauli)

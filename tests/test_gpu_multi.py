@@ -89,3 +89,67 @@ def test_group_errors():
     gp = capi.GroupPlan(grp, gates, 4, npar, 2, 0, 2, pauli)
     with pytest.raises(capi.QfInvalidArgument):
         gp.gradient(theta[:-1])
+
+
+# ---- the multi-process data-parallel path at world_size 2 (both ranks on the
+# one visible B200, process group over gloo): DataParallelGradient, the product
+# path of bench.py under torchrun, with real shards and a real exchange.
+def _free_port():
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _torchrun(args, env_extra, timeout=600):
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, QF_DIST_BACKEND="gloo", OMP_NUM_THREADS="1", **env_extra)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes", "1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port())] + args
+    return subprocess.run(cmd, capture_output=True, text=True, timeout=timeout, env=env)
+
+
+def test_data_parallel_gradient_world2(oracle, tmp_path):
+    import os
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = str(tmp_path / "dp.npz")
+    r = _torchrun([os.path.join(root, "tests", "dp_worker.py")], {"QF_DP_OUT": out})
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    d = np.load(out)
+    n, layers, batch = 14, 4, 7
+    gates, npar = C.build_hea(n, layers)
+    M = npar
+    # the all-reduced shard sums == the single-device gradient of the whole batch
+    # (same per-sample kernels; only the fp64 order of the K sums differs)
+    assert rel_diff(d["red"][:M], d["single_grad"]) <= 1e-6
+    assert abs(d["red"][M] - d["single_loss"]) <= 1e-6 * float(np.abs(d["single_expect"]).sum())
+    np.testing.assert_allclose(d["expect"], d["single_expect"], rtol=0, atol=1e-12)
+    # and the oracle on the same global stream
+    psi0 = C.new_random_state(n, batch, 1234)
+    theta = C.random_parameters(npar, 1235)
+    loss, grad, exp = oracle.gradient(gates, n, npar, psi0, theta,
+                                      C.parse_pauli(C.repeated_ixyz_label(n)))
+    assert rel_diff(d["red"][:M], grad) <= TOL
+    assert abs(d["red"][M] - loss) <= TOL * float(np.abs(exp).sum())
+
+
+def test_bench_two_ranks_gloo():
+    """bench.py launched exactly like the driver's scaling run (torchrun, 2
+    ranks), weak and strong, on a small workload: one JSON line from rank 0,
+    max-over-ranks timing, n_gpus = 2."""
+    import json
+    import os
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    for scaling, batch, glob in (("weak", 8, 16), ("strong", 16, 16)):
+        r = _torchrun([os.path.join(root, "bench.py"), "--gpus", "2", "--steps", "3", "--warmup", "3",
+                       "--workload", "hea16q", "--batch", str(batch), "--layers", "20",
+                       "--scaling", scaling, "--no-cpu", "--no-secondary", "--no-refsig"], {})
+        assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+        lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+        assert len(lines) == 1, r.stdout
+        line = json.loads(lines[0])
+        assert line["n_gpus"] == 2 and line["scaling"] == scaling
+        assert line["config"]["global_batch"] == glob and line["config"]["batch_per_gpu"] == 8
+        assert line["value"] > 0 and line["e2e"]["value"] > 0

@@ -154,10 +154,13 @@ def test_errors(ctx):
         capi.Plan(ctx, g26, 26, np26, 1, 0, 1 << 12, C.parse_pauli("Z" * 26))
 
 
-@pytest.mark.parametrize("n,layers,batch", [(4, 3, 5), (12, 2, 2), (12, 5, 3), (14, 2, 2), (17, 2, 1)])
+@pytest.mark.parametrize("n,layers,batch", [(4, 3, 5), (12, 2, 2), (12, 5, 3), (14, 2, 2), (17, 2, 1),
+                                            (20, 2, 1)])
 def test_forward_state_matches_reference(ctx, ref, n, layers, batch):
-    """Final state of the fused forward vs the reference's forward<double>,
-    up to one global phase per sample (the device drops e^{i delta})."""
+    """Final state of the fused forward vs the reference's forward<double>
+    (engine.hpp:131-133), amplitude for amplitude: the device model's dropped
+    global phase e^{i sum delta} is restored in the readout (no phase is
+    divided out here)."""
     gates, npar, theta, psi0, pauli = _hea_case(n, layers, batch, seed=41)
     plan = capi.Plan(ctx, gates, n, npar, layers, 0, batch, pauli)
     plan.upload_psi0(psi0)
@@ -166,15 +169,28 @@ def test_forward_state_matches_reference(ctx, ref, n, layers, batch):
     g = got[..., 0] + 1j * got[..., 1]
     w = want[..., 0] + 1j * want[..., 1]
     for s in range(batch):
-        ov = np.vdot(g[s], w[s])
-        assert abs(abs(ov) - 1.0) < 1e-5
-        ph = ov / abs(ov)
-        assert np.max(np.abs(g[s] * ph - w[s])) < 1e-5
+        assert np.max(np.abs(g[s] - w[s])) < 1e-5 * max(1.0, 2 ** ((20 - n) / 2) / 32)
+        assert abs(np.vdot(g[s], w[s]) - 1.0) < 1e-5
 
 
-@pytest.mark.parametrize("n,layers,batch", [(21, 1, 1), (22, 2, 1)])
+def test_forward_state_random_circuit_phase(ctx, ref):
+    """Random Rx/Ry/Rz/CZ/CNOT circuit: sections with every axis mix and CNOT
+    Hadamards, the global phase restored exactly."""
+    n = 13
+    gates, npar = C.random_circuit(n, 120, 17)
+    theta = C.random_parameters(npar, 18)
+    psi0 = C.new_random_state(n, 2, 19)
+    plan = capi.Plan(ctx, gates, n, npar, 0, 0, 2, C.parse_pauli("Z" * n))
+    plan.upload_psi0(psi0)
+    got = plan.forward_state(theta).astype(np.float64)
+    want = ref.forward(gates, n, npar, psi0.astype(np.float64), theta)
+    assert np.max(np.abs(got - want)) < 1e-5
+
+
+@pytest.mark.parametrize("n,layers,batch", [(21, 1, 1), (22, 2, 1), (23, 1, 1), (24, 1, 1)])
 def test_three_layouts(ctx, oracle, n, layers, batch):
-    """n > 20 needs a third layout (two passes per stage)."""
+    """n > 20 needs a third layout (two passes per stage); n = 21..24 also take
+    the column-group move of the last layout (qf_plan.cpp)."""
     gates, npar, theta, psi0, pauli = _hea_case(n, layers, batch, seed=8)
     res = capi.gradient_c64(ctx, gates, n, npar, layers, 0, psi0, theta, pauli)
     _check(res, oracle.gradient(gates, n, npar, psi0, theta, pauli))
@@ -188,16 +204,18 @@ def test_streaming_checkpoint_slots(ctx, oracle, k):
     _check(res, oracle.gradient(gates, n, npar, psi0, theta, pauli))
 
 
-def test_device_random_state(ctx):
-    """qf_plan_random_psi0 == new_random_state<float> (statevec.cpp:32-53)."""
-    n, batch = 13, 3
+@pytest.mark.parametrize("n,batch,first", [(13, 3, 5), (16, 2, 3), (4, 9, 0)])
+def test_device_random_state(ctx, ref, n, batch, first):
+    """qf_plan_random_psi0 == new_random_state<float> (statevec.cpp:32-53) bit
+    for bit: the SplitMix64 stream jumped ahead to sample `first`, Box-Muller in
+    fp64, the per-sample norm summed sequentially in amplitude order."""
     gates, npar = C.build_hea(n, 1)
     plan = capi.Plan(ctx, gates, n, npar, 1, 0, batch, C.parse_pauli("Z" * n))
-    plan.random_psi0(1234, first_sample=5)
+    plan.random_psi0(1234, first_sample=first)
     host = np.empty((batch, 1 << n, 2), np.float32)
     plan.download_psi0_ptr(host.ctypes.data)
-    want = C.new_random_state(n, 5 + batch, 1234)[5:]
-    np.testing.assert_allclose(host, want, rtol=0, atol=2e-7)
+    want = ref.random_state(n, first + batch, 1234, np.float32)[first:]  # the reference itself
+    np.testing.assert_array_equal(host.view(np.uint32), want.view(np.uint32))
 
 
 def test_cpp_dropin_shim():
@@ -273,7 +291,9 @@ def test_ragged_batches(ctx, oracle, n, batch):
 
 
 def test_device_psi0_and_device_outputs(ctx, oracle):
-    """qf_plan_set_psi0_device + qf_plan_gradient_device (the data-parallel path)."""
+    """qf_plan_set_psi0_device (aliased caller memory, read in place) +
+    qf_plan_gradient_device (the data-parallel path); a caller that rewrites its
+    buffer between calls gets the gradient of the new contents."""
     torch = pytest.importorskip("torch")
     n, layers, batch = 13, 2, 3
     gates, npar, theta, psi0, pauli = _hea_case(n, layers, batch, seed=12)
@@ -282,13 +302,73 @@ def test_device_psi0_and_device_outputs(ctx, oracle):
     d_theta = torch.from_numpy(theta).cuda()
     out = torch.empty(npar + 1 + batch, dtype=torch.float64, device="cuda")
     plan.set_psi0_device(d_psi.data_ptr())
-    plan.gradient_device(d_theta.data_ptr(), out.data_ptr())
-    plan.synchronize()
-    o = out.cpu().numpy()
-    loss, grad, exp = oracle.gradient(gates, n, npar, psi0, theta, pauli)
-    assert rel_diff(o[:npar], grad) <= TOL
-    assert abs(o[npar] - loss) <= TOL * max(1.0, float(np.sum(np.abs(exp))))
-    assert rel_diff(o[npar + 1:], exp) <= TOL
+    for psi in (psi0, C.new_random_state(n, batch, 4321)):
+        d_psi.copy_(torch.from_numpy(psi))
+        torch.cuda.synchronize()  # the caller orders its write before the plan stream reads
+        plan.gradient_device(d_theta.data_ptr(), out.data_ptr())
+        plan.synchronize()
+        o = out.cpu().numpy()
+        loss, grad, exp = oracle.gradient(gates, n, npar, psi, theta, pauli)
+        assert rel_diff(o[:npar], grad) <= TOL
+        assert abs(o[npar] - loss) <= TOL * max(1.0, float(np.sum(np.abs(exp))))
+        assert rel_diff(o[npar + 1:], exp) <= TOL
+    # never written: the caller's buffer still holds the last input
+    np.testing.assert_array_equal(d_psi.cpu().numpy(), C.new_random_state(n, batch, 4321))
+    # upload_psi0 goes back to the plan's own store
+    plan.upload_psi0(psi0)
+    _check(plan.gradient(theta), oracle.gradient(gates, n, npar, psi0, theta, pauli))
+
+
+@pytest.mark.parametrize("n,batch", [(5, 3), (14, 3)])
+def test_device_psi0_alias_resident_and_streaming(ctx, oracle, n, batch):
+    torch = pytest.importorskip("torch")
+    gates, npar, theta, psi0, pauli = _hea_case(n, 3, batch, seed=14)
+    plan = capi.Plan(ctx, gates, n, npar, 3, 0, batch, pauli)
+    d_psi = torch.from_numpy(psi0).cuda()
+    plan.set_psi0_device(d_psi.data_ptr())
+    _check(plan.gradient(theta), oracle.gradient(gates, n, npar, psi0, theta, pauli))
+
+
+def test_oneshot_plan_cache(ctx, oracle):
+    """Repeated one-shot calls (the reference-signature path) reuse the cached
+    plan: new psi0 and theta every call, a different shape in between, and the
+    cache switched off -- every result against the oracle."""
+    n, layers, batch = 16, 3, 3
+    gates, npar, theta, psi0, pauli = _hea_case(n, layers, batch, seed=71)
+    first = capi.gradient_c64(ctx, gates, n, npar, layers, 1, psi0, theta, pauli)
+    _check(first, oracle.gradient(gates, n, npar, psi0, theta, pauli))
+    psi1 = C.new_random_state(n, batch, 72)
+    th1 = C.random_parameters(npar, 73)
+    again = capi.gradient_c64(ctx, gates, n, npar, layers, 1, psi1, th1, pauli)
+    _check(again, oracle.gradient(gates, n, npar, psi1, th1, pauli))
+    g2, np2, t2, p2, pa2 = _hea_case(13, 2, 2, seed=74)
+    _check(capi.gradient_c64(ctx, g2, 13, np2, 2, 0, p2, t2, pa2),
+           oracle.gradient(g2, 13, np2, p2, t2, pa2))
+    same = capi.gradient_c64(ctx, gates, n, npar, layers, 1, psi0, theta, pauli)
+    np.testing.assert_array_equal(same.gradient, first.gradient)
+    ctx.set_plan_cache(False)
+    try:
+        off = capi.gradient_c64(ctx, gates, n, npar, layers, 1, psi0, theta, pauli)
+        np.testing.assert_array_equal(off.gradient, first.gradient)
+    finally:
+        ctx.set_plan_cache(True)
+
+
+def test_oneshot_staged_large_psi0(ctx, oracle):
+    """psi0 of 64 MiB (> the 8 MiB direct-copy threshold): staged through the
+    pinned buffer in 16 MiB chunks by host threads; pinned sources go direct."""
+    torch = pytest.importorskip("torch")
+    n, layers, batch = 20, 1, 8
+    gates, npar, theta, psi0, pauli = _hea_case(n, layers, batch, seed=75)
+    res = capi.gradient_c64(ctx, gates, n, npar, layers, 0, psi0, theta, pauli)
+    plan = capi.Plan(ctx, gates, n, npar, layers, 0, batch, pauli)
+    plan.upload_psi0(psi0)
+    ref_plan = plan.gradient(theta)
+    plan.close()
+    np.testing.assert_array_equal(res.gradient, ref_plan.gradient)
+    pinned = torch.from_numpy(psi0).pin_memory()
+    res2 = capi.gradient_c64(ctx, gates, n, npar, layers, 0, pinned.numpy(), theta, pauli)
+    np.testing.assert_array_equal(res2.gradient, ref_plan.gradient)
 
 
 def test_deep_circuit_uncompute_drift(ctx, oracle):
@@ -300,12 +380,12 @@ def test_deep_circuit_uncompute_drift(ctx, oracle):
 
 
 def test_config4_depth_fused_vs_pergate(ctx):
-    """BASELINE config 4 depth (20q x 1000 layers, k = 10) on a 2-sample shard:
+    """BASELINE config 4 depth (20q x 1000 layers, k = 10) on a 4-sample shard:
     the fused path (X, Y measured, Z chained over 1000 stages, scales folded
     into the diagonals) against the independent per-gate comparator (one
     kernel per gate, 80,000 gates each way). The CPU oracle would need ~10 min
     here, so this is the size-independent cross-check at full depth."""
-    n, layers, batch = 20, 1000, 2
+    n, layers, batch = 20, 1000, 4
     gates, npar, theta, psi0, pauli = _hea_case(n, layers, batch, seed=4242)
     fused = capi.gradient_c64(ctx, gates, n, npar, layers, 10, psi0, theta, pauli)
     pg = capi.gradient_c64(ctx, gates, n, npar, layers, 0, psi0, theta, pauli, pergate=True)
@@ -496,28 +576,92 @@ def test_c128_errors(ctx):
         capi.gradient_c128(ctx, gates, 4, npar, 2, 3, psi0, theta, pauli)
 
 
-def test_cpp_bench_driver():
-    """qfuse::b200::run_bench / scan_blocks (the reference's bench API on the B200)
-    against the reference's run_bench on the same BenchConfig; the reference's
-    JSON/CSV serialisers round-trip our BenchReport; the CLI prints its JSON."""
-    import json
+def _drivers():
     import os
-    import subprocess
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    exe = os.path.join(root, "build", "tests", "bench_driver")
-    if not os.path.exists(exe):
-        pytest.skip("build/tests/bench_driver not built (needs the reference sources at build time)")
-    r = subprocess.run([exe], capture_output=True, text=True, timeout=900)
-    print(r.stdout)
+    b200 = os.path.join(root, "build", "tests", "bench_driver")
+    cpu = os.path.join(root, "build", "tests", "bench_driver_ref")
+    if not (os.path.exists(b200) and os.path.exists(cpu)):
+        pytest.skip("build/tests/bench_driver* not built (needs the reference sources at build time)")
+    return b200, cpu
+
+
+def _run(cmd, timeout=900):
+    import subprocess
+    return subprocess.run(cmd, capture_output=True, text=True, timeout=timeout)
+
+
+@pytest.mark.parametrize("flags,tol", [
+    (["--qubits", "4", "--layers", "4", "--batch", "8"], 1e-4),                       # config 1
+    (["--qubits", "4", "--layers", "4", "--batch", "8", "--mode", "naive"], 1e-4),
+    (["--qubits", "4", "--layers", "4", "--batch", "8", "--precision", "double"], 1e-10),
+    (["--qubits", "12", "--layers", "20", "--batch", "4", "--block", "10"], 1e-4),
+    (["--qubits", "16", "--layers", "4", "--batch", "2", "--block", "2", "--mode", "fused_mem_save"], 5e-3),
+    (["--qubits", "8", "--layers", "2", "--shape-qubits", "20"], 1e-4),               # build_hea_shape
+])
+def test_cpp_bench_driver_vs_reference(flags, tol):
+    """The reference's own host driver (bench.cpp run_bench, unmodified) linked
+    against the B200 engine drop-in vs the same driver linked against the
+    reference engine, same flags: loss and gradient checksum agree; the report
+    schema is the reference's."""
+    import json
+    b200, cpu = _drivers()
+    common = ["--reps", "1", "--warmup", "1"]
+    r1, r2 = _run([b200] + flags + common), _run([cpu] + flags + common)
+    assert r1.returncode == 0, r1.stderr
+    assert r2.returncode == 0, r2.stderr
+    ours, ref = json.loads(r1.stdout), json.loads(r2.stdout)
+    assert ours["config"] == ref["config"]
+    o, r = ours["results"], ref["results"]
+    scale = max(1.0, abs(r["loss"]))
+    assert abs(o["loss"] - r["loss"]) <= tol * scale, (o["loss"], r["loss"])
+    assert abs(o["gradient_checksum"] - r["gradient_checksum"]) <= tol * max(1.0, abs(r["gradient_checksum"]))
+    assert o["throughput_sps"] > 0
+
+
+def test_cpp_bench_driver_cli():
+    """Self-test (the reference's JSON/CSV serialisers round-trip this build's
+    reports), scan-blocks, exit codes (qfuse_bench_main.cpp:110-116), --gpus 1
+    (qf_gradient_c64_multi path) and --device."""
+    import json
+    b200, _ = _drivers()
+    r = _run([b200, "--selftest"])
     assert r.returncode == 0 and "ALL PASSED" in r.stdout, r.stdout + r.stderr
-    r = subprocess.run([exe, "--qubits", "16", "--layers", "20", "--batch", "8", "--block", "10",
-                        "--reps", "2", "--warmup", "1"], capture_output=True, text=True, timeout=600)
+    r = _run([b200, "--qubits", "16", "--layers", "20", "--batch", "8", "--block", "10",
+              "--reps", "2", "--warmup", "1"])
     assert r.returncode == 0, r.stderr
     rep = json.loads(r.stdout)
     assert rep["config"]["qubits"] == 16 and rep["results"]["throughput_sps"] > 0
-    r = subprocess.run([exe, "--qubits", "4", "--layers", "3", "--block", "2"],
-                       capture_output=True, text=True, timeout=60)
-    assert r.returncode == 2  # config error exit code (qfuse_bench_main.cpp:110-116)
+    single = rep["results"]
+    r = _run([b200, "--qubits", "16", "--layers", "20", "--batch", "8", "--block", "10",
+              "--reps", "1", "--warmup", "0", "--gpus", "1"])
+    assert r.returncode == 0, r.stderr
+    multi = json.loads(r.stdout)["results"]
+    assert abs(multi["loss"] - single["loss"]) <= 1e-12 * max(1.0, abs(single["loss"]))
+    r = _run([b200, "--qubits", "6", "--layers", "8", "--batch", "2", "--scan-blocks", "1,2,4",
+              "--format", "csv", "--device", "0"])
+    assert r.returncode == 0 and len(r.stdout.strip().splitlines()) == 4, r.stdout + r.stderr
+    assert _run([b200, "--qubits", "4", "--layers", "3", "--block", "2"]).returncode == 2
+    assert _run([b200, "--bogus"]).returncode == 2
+    assert _run([b200, "--qubits", "30", "--layers", "2", "--batch", "1024"]).returncode == 3
+
+
+def test_golden_state_exchange_qsv1(tmp_path):
+    """Golden-state exchange in the reference's QSV1 format: the B200 driver
+    writes forward<float> final states with the reference's dump_state, the
+    CPU-reference driver loads them with load_state and checks them against its
+    own forward<float> (statevec.cpp:122-186, engine.hpp:131-133); and back."""
+    b200, cpu = _drivers()
+    g1, g2 = str(tmp_path / "b200.qsv"), str(tmp_path / "ref.qsv")
+    wl = ["--qubits", "14", "--layers", "6", "--batch", "3"]
+    r = _run([b200] + wl + ["--golden-out", g1])
+    assert r.returncode == 0, r.stderr
+    r = _run([cpu] + wl + ["--golden-check", g1, "--golden-out", g2])
+    assert r.returncode == 0, r.stdout + r.stderr
+    r = _run([b200] + wl + ["--golden-check", g2])
+    assert r.returncode == 0, r.stdout + r.stderr
+    with open(g1, "rb") as f:
+        assert f.read(4) == b"QSV1"
 
 
 def test_config3_depth_subset_vs_oracle(ctx, oracle):
@@ -537,4 +681,23 @@ def test_config4_shape_vs_oracle(ctx, oracle):
     n, layers, batch = 20, 40, 1
     gates, npar, theta, psi0, pauli = _hea_case(n, layers, batch, seed=1234)
     res = capi.gradient_c64(ctx, gates, n, npar, layers, 10, psi0, theta, pauli)
+    _check(res, oracle.gradient(gates, n, npar, psi0, theta, pauli))
+
+
+def test_config2_depth_vs_oracle(ctx, oracle):
+    """BASELINE config 2 shape (12q x 100 layers, k = 10) on a 4-sample subset:
+    the chained sample-resident kernel over 100 stages with 10 slot splits,
+    against the fp64 oracle."""
+    n, layers, batch = 12, 100, 4
+    gates, npar, theta, psi0, pauli = _hea_case(n, layers, batch, seed=1234)
+    res = capi.gradient_c64(ctx, gates, n, npar, layers, 10, psi0, theta, pauli)
+    _check(res, oracle.gradient(gates, n, npar, psi0, theta, pauli))
+
+
+@pytest.mark.parametrize("n", [17, 18, 19])
+def test_hea_17_19_deep_vs_oracle(ctx, oracle, n):
+    """HEA n = 17..19 (streaming, layouts A/B with 5..7 top qubits rotated in
+    B) at 20 layers, k = 10, against the fp64 oracle."""
+    gates, npar, theta, psi0, pauli = _hea_case(n, 20, 1, seed=300 + n)
+    res = capi.gradient_c64(ctx, gates, n, npar, 20, 10, psi0, theta, pauli)
     _check(res, oracle.gradient(gates, n, npar, psi0, theta, pauli))
