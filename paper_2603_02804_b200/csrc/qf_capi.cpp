@@ -177,6 +177,11 @@ struct qf_plan {
     double *theta = nullptr, *out = nullptr;
     float2 *ry = nullptr;
     DiagTab *dtab = nullptr;
+    DiagTabW *dtabw = nullptr; // wide-group tables (layout 0), nullptr when !P.wide
+    CzTabW *cztabw = nullptr;
+    uint32_t *tileinfow = nullptr;
+    std::vector<size_t> tileinfow_off; // [czset]
+    int *dqw = nullptr;
     double *wg = nullptr, *wa = nullptr, *wfinal = nullptr, *sec_gamma = nullptr, *sec_phase = nullptr;
     // theta-independent tables
     CzTab *cztab = nullptr;
@@ -324,6 +329,17 @@ void build_device_plan(qf_plan *pl) {
     pl->wfinal = dalloc<double>(n + 1, o); // [n]: global phase (forward-state readout)
     ck(cudaMemset(pl->wfinal, 0, (n + 1) * sizeof(double)), "memset");
     pl->dtab = dalloc<DiagTab>(std::max<uint32_t>(S, 1), o);
+    if (P.wide) {
+        pl->dtabw = dalloc<DiagTabW>(std::max<uint32_t>(S, 1), o);
+        pl->cztabw = P.cztabw.empty() ? nullptr : dupload(P.cztabw, o);
+        std::vector<uint32_t> tw;
+        for (const auto &t : P.tileinfow) {
+            pl->tileinfow_off.push_back(tw.size());
+            tw.insert(tw.end(), t.begin(), t.end());
+        }
+        pl->tileinfow = tw.empty() ? nullptr : dupload(tw, o);
+        pl->dqw = dupload(std::vector<int>(P.dqw, P.dqw + 28), o);
+    }
     pl->sec_gamma = dalloc<double>(P.sec_q.size(), o);
     pl->sec_phase = dalloc<double>(P.sec_q.size(), o);
     pl->cztab = dupload(P.cztab, o);
@@ -416,6 +432,10 @@ void enqueue_prep(qf_plan *pl, const double *theta_dev, qf_stats &st) {
         ck(launch_diag_tables(s, int(P.stages), int(P.n), pl->wg, pl->wa, pl->stage_layout, pl->dq,
                               pl->dtab, pl->wfinal),
            "diag_tables");
+        if (P.wide)
+            ck(launch_diag_tables_wide(s, int(P.stages), int(P.n), pl->wg, pl->wa, pl->stage_layout, pl->dqw,
+                                       pl->dtabw),
+               "diag_tables_wide");
     });
     st.kernel_launches += 2;
 }
@@ -442,6 +462,12 @@ PassParams pass_params(qf_plan *pl, const PassStep &ps, bool write_psi) {
         p.cz = c >= 0 ? pl->cztab + size_t(c) * P.layouts.size() + ps.layout : nullptr;
         p.tileinfo = c >= 0 ? pl->tinfo(c, ps.layout) : nullptr;
     }
+    if (P.wide && ps.layout == 0 && ps.sd >= 0) {
+        p.dtw = pl->dtabw + ps.sd;
+        const int c = P.stage_cz[ps.sd];
+        p.czw = c >= 0 ? pl->cztabw + c : nullptr;
+        p.tileinfow = c >= 0 ? pl->tileinfow + pl->tileinfow_off[c] : nullptr;
+    }
     p.write_psi = write_psi ? 1 : 0;
     p.zmask = (ps.s0 == 0 ? 1 : 0) | (ps.s1 == 0 ? 2 : 0);
     p.prog = prog_encode(p.nph, p.ph, p.rot_mask);
@@ -450,6 +476,11 @@ PassParams pass_params(qf_plan *pl, const PassStep &ps, bool write_psi) {
         return e ? atoi(e) : 1;
     }();
     p.l2pf = l2pf;
+    static const int wrefill = [] { // wide forward: refill at the next tile's start (2) or at its
+        const char *e = getenv("QF_WREFILL"); // first phase boundary (0, measured faster)
+        return e ? atoi(e) : 0;
+    }();
+    if (p.dtw) p.l2pf = (p.l2pf & 1) | wrefill;
     p.kpart = pl->kpart;
     p.kstride = (long long)P.stages * P.n * 8;
     return p;
@@ -516,9 +547,9 @@ void enqueue_fused(qf_plan *pl, const double *theta_dev, double *out_dev, qf_sta
             const CUtensorMap *outm = (!ms && P.slot_pass(pi)) ? &pl->m_slot[pi / P.ckpt_passes][ps.layout]
                                                                : &pl->m_W[ps.layout];
             PassParams p = pass_params(pl, ps, true);
-            pl->timed(0, 2 * sb, [&] {
-                ck(launch_pass(s, false, std::min(pl->grid_fwd, p.tiles), p, in, outm, nullptr), "pass fwd");
-            });
+            const int grid = pass_is_wide(false, p) ? std::min(wide_grid(pl->ctx->sms), p.tiles)
+                                                    : std::min(pl->grid_fwd, p.tiles);
+            pl->timed(0, 2 * sb, [&] { ck(launch_pass(s, false, grid, p, in, outm, nullptr), "pass fwd"); });
             st.kernel_launches++;
             st.forward_passes++;
             bytes += 2 * sb;

@@ -53,6 +53,24 @@ struct CzTab {
     uint16_t thrinfo[256];
 };
 
+// Wide-group view of layout A (forward passes, qf_pass_wide.cu): a thread holds
+// 64 amplitudes, the 6 local bits {0,1,2,3,7,8} (group L) or {4,5,6,9,10,11}
+// (group H) in registers. The diagonal is applied in group L: its register bits
+// (treg[64]) and the 6 thread bits (tthr[64]); the tile terms are DiagTab's.
+__host__ __device__ constexpr int wide_reg_bit(int b) { return b < 4 ? b : b + 3; } // 0,1,2,3,7,8
+__host__ __device__ constexpr int wide_thr_bit(int b) { return b < 3 ? b + 4 : b + 6; } // 4,5,6,9,10,11
+struct DiagTabW {
+    float2 treg[64];
+    float2 tthr[64];
+};
+// CZ signs in the wide L view: sgn (64 bits) = (sbase ? ~0 : 0) ^ qreg ^ linmask6(M),
+// sbase = Q(tile) ^ Q(thr) ^ parity(tau & Rtile), M = Mtile ^ Mthr;
+// thrinfo[tau] = Q(thr) << 6 | Mthr;  tileinfo[tb] = Q(tile) | Mtile << 1 | Rtile << 8.
+struct CzTabW {
+    unsigned long long qreg;
+    uint16_t thrinfo[64];
+};
+
 // Adjacency of a CZ set, for the observable fold (seed).
 struct CzAdj {
     uint32_t adjlo[32]; // bit p < q of adjlo[q] = CZ(p, q)
@@ -103,6 +121,10 @@ struct PassParams {
     const DiagTab *dt; // diagonal of this pass (nullptr = none)
     const CzTab *cz;   // its CZ set in this layout (nullptr = none)
     const uint32_t *tileinfo;
+    // wide-group forward of layout A (nullptr: not available for this pass)
+    const DiagTabW *dtw;
+    const CzTabW *czw;
+    const uint32_t *tileinfow;
     int write_psi;     // backward: store psi (0 when the next reader is a slot)
     int zmask;         // backward: bit r = round r measures Z (its stage is 0)
     uint32_t prog;     // prog_encode(nph, ph, rot_mask)
@@ -159,6 +181,17 @@ cudaError_t launch_phase_sum(cudaStream_t st, int n_sec, const double *sec_phase
 cudaError_t launch_diag_tables(cudaStream_t st, int stages, int n, const double *wg,
                                const double *wa, const int *stage_layout, const int *dq,
                                DiagTab *dt, double *wfinal);
+// Wide-group tables of the stages layout 0 applies (stage_layout[s] == 0), from the
+// wide view dqw[0..5] reg bits, [6..11] thread bits (qubits, -1 = none).
+cudaError_t launch_diag_tables_wide(cudaStream_t st, int stages, int n, const double *wg,
+                                    const double *wa, const int *stage_layout, const int *dqw,
+                                    DiagTabW *dtw);
+int wide_grid(int sms);
+// The forward pass runs the wide kernel (interior layout-A pass with wide tables);
+// its grid is wide_grid(sms) instead of the narrow kernels' occupancy x sms.
+bool pass_is_wide(bool backward, const PassParams &p);
+cudaError_t launch_pass_wide(cudaStream_t st, int grid, const PassParams &p, const CUtensorMap *psi_in,
+                             const CUtensorMap *psi_out);
 cudaError_t launch_pass(cudaStream_t st, bool backward, int grid, const PassParams &p,
                         const CUtensorMap *psi_in, const CUtensorMap *psi_out,
                         const CUtensorMap *lam);

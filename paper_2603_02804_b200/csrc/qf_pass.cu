@@ -426,9 +426,18 @@ int pass_occupancy(bool backward) {
     return blocks;
 }
 
+bool pass_is_wide(bool backward, const PassParams &p) {
+    static const bool enabled = [] {
+        const char *e = getenv("QF_WIDE"); // QF_WIDE=0: narrow kernels only (A/B timing)
+        return !e || atoi(e) != 0;
+    }();
+    return enabled && !backward && p.dtw != nullptr && progs_enabled() && p.prog == kProgA;
+}
+
 cudaError_t launch_pass(cudaStream_t st, bool backward, int grid, const PassParams &p,
                         const CUtensorMap *psi_in, const CUtensorMap *psi_out,
                         const CUtensorMap *lam) {
+    if (pass_is_wide(backward, p)) return launch_pass_wide(st, grid, p, psi_in, psi_out);
     cudaError_t e = ensure_attrs();
     if (e != cudaSuccess) return e;
     const CUtensorMap &l = lam ? *lam : *psi_out;

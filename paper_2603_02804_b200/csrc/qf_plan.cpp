@@ -276,6 +276,51 @@ Plan make_plan(const qf_gate *gates, size_t n_gates, uint32_t n, uint32_t n_para
         }
     }
 
+    // ---- wide-group view of layout A (forward passes rotating all 12 local qubits)
+    if (!plan.resident && plan.layouts[0].rot_mask == 0xFFFu) {
+        const PassLayout &L = plan.layouts[0];
+        plan.wide = true;
+        for (int i = 0; i < 28; ++i) plan.dqw[i] = -1;
+        for (int b = 0; b < 6; ++b) {
+            plan.dqw[b] = L.qmap[wide_reg_bit(b)];
+            plan.dqw[6 + b] = L.qmap[wide_thr_bit(b)];
+        }
+        for (size_t i = 0; i < L.tile_qubits.size() && i < 16; ++i) plan.dqw[12 + i] = L.tile_qubits[i];
+        for (size_t c = 0; c < adjs.size(); ++c) {
+            const auto &adj = adjs[c];
+            auto qset = [&](const int *qs, int k, uint32_t v) {
+                uint32_t par = 0;
+                for (int i = 0; i < k; ++i) {
+                    if (!((v >> i) & 1u) || qs[i] < 0) continue;
+                    for (int j = i + 1; j < k; ++j)
+                        if (((v >> j) & 1u) && qs[j] >= 0) par ^= (adj[qs[i]] >> qs[j]) & 1u;
+                }
+                return par;
+            };
+            auto cross = [&](const int *qs, int k, uint32_t v, const int *to, int kto) {
+                uint32_t m = 0;
+                for (int i = 0; i < k; ++i) {
+                    if (!((v >> i) & 1u) || qs[i] < 0) continue;
+                    for (int r = 0; r < kto; ++r)
+                        if (to[r] >= 0) m ^= ((adj[qs[i]] >> to[r]) & 1u) << r;
+                }
+                return m;
+            };
+            const int *reg = plan.dqw, *thr = plan.dqw + 6;
+            CzTabW ct{};
+            for (uint32_t j = 0; j < 64; ++j) ct.qreg |= (unsigned long long)qset(reg, 6, j) << j;
+            for (uint32_t tau = 0; tau < 64; ++tau)
+                ct.thrinfo[tau] = static_cast<uint16_t>((qset(thr, 6, tau) << 6) | cross(thr, 6, tau, reg, 6));
+            plan.cztabw.push_back(ct);
+            const int kt = static_cast<int>(L.tile_qubits.size());
+            std::vector<uint32_t> ti(size_t(1) << kt);
+            for (uint32_t tb = 0; tb < ti.size(); ++tb)
+                ti[tb] = qset(L.tile_qubits.data(), kt, tb) | (cross(L.tile_qubits.data(), kt, tb, reg, 6) << 1) |
+                         (cross(L.tile_qubits.data(), kt, tb, thr, 6) << 8);
+            plan.tileinfow.push_back(std::move(ti));
+        }
+    }
+
     // ---- pass sequence (streaming): a pass on layout X applies Ry_{r[X]}(X); when
     // every layout has finished stage dnext-1 it also applies D_{dnext} and, on
     // its own qubits, Ry_{dnext}. Two layouts -> one pass per stage.

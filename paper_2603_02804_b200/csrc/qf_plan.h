@@ -58,6 +58,12 @@ struct Plan {
     std::vector<CzTab> cztab;      // [czset][layout]
     std::vector<std::vector<uint32_t>> tileinfo; // [czset][layout]
     std::vector<CzAdj> final_adj;  // 0 or 1 entries
+    // wide-group view of layout 0 (forward passes with all 12 local qubits rotated,
+    // qf_pass_wide.cu): dqw[0..5] register bits, [6..11] thread bits, [12..] tile bits
+    bool wide = false;
+    int dqw[28] = {};
+    std::vector<CzTabW> cztabw;                   // [czset]
+    std::vector<std::vector<uint32_t>> tileinfow; // [czset]
     uint32_t ckpt_stages = 1;      // k in stages
     uint32_t ckpt_layers = 0;      // k in layers as reported
     uint32_t ckpt_passes = 1;      // k in passes (streaming)

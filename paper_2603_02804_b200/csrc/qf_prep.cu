@@ -141,6 +141,23 @@ __global__ void diag_tables_kernel(int stages, int n, const double *wg, const do
     }
 }
 
+// Wide-group register/thread tables (qf_pass_wide.cu) of the stages layout 0 applies.
+__global__ void diag_tables_wide_kernel(int n, const double *wg, const double *wa,
+                                        const int *stage_layout, const int *dqw, DiagTabW *dtw) {
+    const int s = blockIdx.x;
+    if (stage_layout[s] != 0) return;
+    const int e = threadIdx.x; // 0..63 register entries, 64..127 thread entries
+    const int base = e < 64 ? 0 : 6, idx = e & 63;
+    double ang = 0.0;
+    for (int b = 0; b < 6; ++b) {
+        const int q = dqw[base + b];
+        if (q >= 0 && q < n && ((idx >> b) & 1)) ang += wg[size_t(s) * n + q] + wa[size_t(s) * n + q];
+    }
+    double sn, cs;
+    sincos(ang, &sn, &cs);
+    (e < 64 ? dtw[s].treg : dtw[s].tthr)[idx] = make_float2(float(cs), float(sn));
+}
+
 // kout[e] = sum over CTAs (fixed order) of kpart[cta][e]; expect[s] = sum of
 // the seed kernel's chunk partials.
 __global__ void reduce_kernel(long long entries, int grid, const double *kpart, double *kout,
@@ -289,6 +306,14 @@ cudaError_t launch_diag_tables(cudaStream_t st, int stages, int n, const double 
                                const double *wa, const int *stage_layout, const int *dq,
                                DiagTab *dt, double *wfinal) {
     diag_tables_kernel<<<stages + 1, 256, 0, st>>>(stages, n, wg, wa, stage_layout, dq, dt, wfinal);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_diag_tables_wide(cudaStream_t st, int stages, int n, const double *wg,
+                                    const double *wa, const int *stage_layout, const int *dqw,
+                                    DiagTabW *dtw) {
+    if (stages == 0) return cudaSuccess;
+    diag_tables_wide_kernel<<<stages, 128, 0, st>>>(n, wg, wa, stage_layout, dqw, dtw);
     return cudaGetLastError();
 }
 

@@ -162,11 +162,16 @@ __global__ void __launch_bounds__(kThreads) seed_kernel(const SeedParams p) {
     }
 }
 
-constexpr size_t kResAcc = size_t(8) * 2 * 12 * 8 * sizeof(double);
-constexpr size_t res_smem() {
-    return size_t(2) * kTileBytes + size_t(kTileAmps) * sizeof(double) + 64 +
-           2 * 24 * 16 /*rys*/ + 2 * 16 * 8 /*treg*/ + 2 * 6 * 8 /*mgs*/ + 64 /*kc, fold*/ + kResAcc +
-           1024;
+// K accumulators per warp: [slots][12 local bits][8]. n < 12: 2 slots (stage
+// parity); n = 12: a 4-slot ring by stage (the chained backward flushes stage s
+// while stage s-1 is still accumulating, without a barrier of its own).
+constexpr int res_kslots(bool n12) { return n12 ? 4 : 2; }
+constexpr size_t res_acc(bool n12) { return size_t(8) * res_kslots(n12) * 12 * 8 * sizeof(double); }
+// n = 12 reduces the expectation in registers (no per-amplitude fp64 scratch).
+constexpr size_t res_es(bool n12) { return n12 ? 64 : size_t(kTileAmps) * sizeof(double); }
+constexpr size_t res_smem(bool n12) {
+    return size_t(2) * kTileBytes + res_es(n12) + 64 + 2 * 24 * 16 /*rys*/ + 2 * 16 * 8 /*treg*/ +
+           2 * 6 * 8 /*mgs*/ + 64 /*kc, fold*/ + res_acc(n12) + 1024;
 }
 
 // N12: n == 12 (every group fully rotated): the phases are compile-time
@@ -181,7 +186,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     uint8_t *smem = align1024(smem_raw);
     uint8_t *pt = smem, *lt = smem + kTileBytes;
     double *es = reinterpret_cast<double *>(smem + 2 * kTileBytes);
-    uint8_t *tail = smem + 2 * kTileBytes + kTileAmps * sizeof(double);
+    uint8_t *tail = smem + 2 * kTileBytes + res_es(N12);
     uint64_t *mbar = reinterpret_cast<uint64_t *>(tail);
     float4 *rys = reinterpret_cast<float4 *>(tail + 64);                  // [2 slots][24]
     float2 *treg_s = reinterpret_cast<float2 *>(tail + 64 + 2 * 24 * 16); // [2 slots][16]
@@ -195,7 +200,8 @@ __global__ void __launch_bounds__(kThreads, 2)
     const uint32_t xmask = rot;
     const int spt = kTileAmps >> (n < 12 ? n : 12);
 
-    for (uint32_t i = tid; i < kResAcc / 8; i += kThreads) acc[i] = 0.0;
+    constexpr int KS = res_kslots(N12);
+    for (uint32_t i = tid; i < res_acc(N12) / 8; i += kThreads) acc[i] = 0.0;
     if (tid < 48) { // round-0 halves stay identity (t = 0, m = 1)
         rys[tid] = make_float4(0.f, 0.f, 1.f, 0.f);
     } else if (tid < 60) {
@@ -255,7 +261,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         e.kc = kc + sl * 6;
         e.zm = s == 0 ? 3u : 0u; // Z at stage 0 only (zchain_kernel rebuilds the rest)
         e.treg_s = treg_s + sl * 16;
-        e.acc_w = acc + warp * 2 * 12 * 8;
+        e.acc_w = acc + warp * KS * 96;
         e.acc_w1 = e.acc_w + 12 * 8;
         const int c = p.stage_cz[s];
         const CzTab *cz = c >= 0 ? p.cztabs + c * p.cz_stride : nullptr;
@@ -318,8 +324,8 @@ __global__ void __launch_bounds__(kThreads, 2)
         e.scale = !fold[b];
         e.scale1 = !fold[b + 1];
         e.zm = (a == 0 ? 1u : 0u) | (a + 1 == 0 ? 2u : 0u);
-        e.acc_w = acc + warp * 2 * 12 * 8 + (a & 1) * 96;
-        e.acc_w1 = acc + warp * 2 * 12 * 8 + ((a + 1) & 1) * 96;
+        e.acc_w = acc + warp * KS * 96 + (a & (KS - 1)) * 96;
+        e.acc_w1 = acc + warp * KS * 96 + ((a + 1) & (KS - 1)) * 96;
         e.treg_s = treg_s + (d & 1) * 16;
         e.d.base = make_float2(1.f, 0.f);
         e.d.sgn = 0;
@@ -423,28 +429,52 @@ __global__ void __launch_bounds__(kThreads, 2)
             continue;
         }
         // ---------------- observable: lambda = 2 O' psi, E per sample
+        if constexpr (N12) { // one sample per tile: thread sums, warp butterfly, fixed warp order
+            double e = 0.0;
 #pragma unroll 4
-        for (int j = 0; j < 16; ++j) {
-            const uint32_t l = (tid << 4) | uint32_t(j);
-            const uint32_t lp = l ^ uint32_t(p.x_mask);
-            const float2 f = seed_factor(l & xmask, p.x_mask, p.z_mask, p.y_count, p.wfinal, p.czfinal);
-            const float2 ps = *reinterpret_cast<const float2 *>(pt + swz(lp));
-            const float2 px = *reinterpret_cast<const float2 *>(pt + swz(l));
-            const float2 lv = cmul(f, ps);
-            *reinterpret_cast<float2 *>(lt + swz(l)) = lv;
-            es[l] = 0.5 * (double(px.x) * double(lv.x) + double(px.y) * double(lv.y));
-        }
-        __syncthreads();
-        for (int st = 1; st < (1 << (n < 12 ? n : 12)); st <<= 1) {
-            for (int i = tid; i < (kTileAmps >> 1) / st; i += kThreads) {
-                const int idx = i * 2 * st;
-                es[idx] += es[idx + st];
+            for (int j = 0; j < 16; ++j) {
+                const uint32_t l = (tid << 4) | uint32_t(j);
+                const uint32_t lp = l ^ uint32_t(p.x_mask);
+                const float2 f = seed_factor(l, p.x_mask, p.z_mask, p.y_count, p.wfinal, p.czfinal);
+                const float2 ps = *reinterpret_cast<const float2 *>(pt + swz(lp));
+                const float2 px = *reinterpret_cast<const float2 *>(pt + swz(l));
+                const float2 lv = cmul(f, ps);
+                *reinterpret_cast<float2 *>(lt + swz(l)) = lv;
+                e += 0.5 * (double(px.x) * double(lv.x) + double(px.y) * double(lv.y));
+            }
+#pragma unroll
+            for (int m = 16; m >= 1; m >>= 1) e += __shfl_xor_sync(0xffffffffu, e, m);
+            if ((tid & 31u) == 0) es[warp] = e;
+            __syncthreads();
+            if (tid == 0) {
+                double sum = 0.0;
+                for (int w = 0; w < 8; ++w) sum += es[w];
+                if (uint32_t(t) < p.batch) p.expect[t] = sum;
+            }
+        } else {
+#pragma unroll 4
+            for (int j = 0; j < 16; ++j) {
+                const uint32_t l = (tid << 4) | uint32_t(j);
+                const uint32_t lp = l ^ uint32_t(p.x_mask);
+                const float2 f = seed_factor(l & xmask, p.x_mask, p.z_mask, p.y_count, p.wfinal, p.czfinal);
+                const float2 ps = *reinterpret_cast<const float2 *>(pt + swz(lp));
+                const float2 px = *reinterpret_cast<const float2 *>(pt + swz(l));
+                const float2 lv = cmul(f, ps);
+                *reinterpret_cast<float2 *>(lt + swz(l)) = lv;
+                es[l] = 0.5 * (double(px.x) * double(lv.x) + double(px.y) * double(lv.y));
             }
             __syncthreads();
-        }
-        for (uint32_t ls = tid; ls < uint32_t(spt); ls += kThreads) { // n < 4: > 256 samples/tile
-            const uint64_t sample = uint64_t(t) * spt + ls;
-            if (sample < p.batch) p.expect[sample] = es[ls << (n < 12 ? n : 12)];
+            for (int st = 1; st < (1 << (n < 12 ? n : 12)); st <<= 1) {
+                for (int i = tid; i < (kTileAmps >> 1) / st; i += kThreads) {
+                    const int idx = i * 2 * st;
+                    es[idx] += es[idx + st];
+                }
+                __syncthreads();
+            }
+            for (uint32_t ls = tid; ls < uint32_t(spt); ls += kThreads) { // n < 4: > 256 samples/tile
+                const uint64_t sample = uint64_t(t) * spt + ls;
+                if (sample < p.batch) p.expect[sample] = es[ls << (n < 12 ? n : 12)];
+            }
         }
         // ---------------- backward
         // K of stage s from accumulator slot ks, added (RED) to this CTA's kpart row
@@ -455,7 +485,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                     double sum = 0.0;
 #pragma unroll
                     for (int w = 0; w < 8; ++w) {
-                        double *a = acc + ((w * 2 + ks) * 12 + lb) * 8 + c;
+                        double *a = acc + ((w * KS + ks) * 12 + lb) * 8 + c;
                         sum += *a;
                         *a = 0.0;
                     }
@@ -500,9 +530,11 @@ __global__ void __launch_bounds__(kThreads, 2)
                     }
                 }
                 __syncthreads();
-                flush_k(s, s & 1);
-                __syncthreads();
+                // stage s is complete (its round-0 part came from iteration s + 1);
+                // its ring slot is next written in iteration s - 3, barriers later
+                flush_k(s, s & (KS - 1));
             }
+            __syncthreads(); // the next tile reuses psi / lambda
         } else {
             if (S > 0) load_stage(S - 1);
             __syncthreads();
@@ -532,20 +564,20 @@ std::atomic<uint64_t> g_attrs{0};
 
 } // namespace
 
-size_t resident_smem_bytes() { return res_smem(); }
+size_t resident_smem_bytes() { return res_smem(true); }
 
 int resident_occupancy() {
     const cudaError_t e = once_per_device(g_attrs, [] {
         cudaError_t r = cudaFuncSetAttribute(resident_kernel<false>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, int(res_smem()));
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, int(res_smem(false)));
         if (r == cudaSuccess)
             r = cudaFuncSetAttribute(resident_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     int(res_smem()));
+                                     int(res_smem(true)));
         return r;
     });
     if (e != cudaSuccess) return 0;
     int blocks = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, resident_kernel<false>, kThreads, res_smem());
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, resident_kernel<false>, kThreads, res_smem(false));
     return blocks;
 }
 
@@ -554,9 +586,9 @@ cudaError_t launch_resident(cudaStream_t st, int grid, const ResidentParams &p,
                             const CUtensorMap *out_map) {
     if (resident_occupancy() <= 0) return cudaErrorInvalidConfiguration;
     if (p.n == 12)
-        resident_kernel<true><<<grid, kThreads, res_smem(), st>>>(p, *psi0, *slots_map, *out_map);
+        resident_kernel<true><<<grid, kThreads, res_smem(true), st>>>(p, *psi0, *slots_map, *out_map);
     else
-        resident_kernel<false><<<grid, kThreads, res_smem(), st>>>(p, *psi0, *slots_map, *out_map);
+        resident_kernel<false><<<grid, kThreads, res_smem(false), st>>>(p, *psi0, *slots_map, *out_map);
     return cudaGetLastError();
 }
 
