@@ -105,6 +105,11 @@ constexpr uint32_t kProgA = prog_encode(5, kProgAPh, 0xFFFu);
 constexpr uint32_t kProgB20 = prog_encode(3, kProgB20Ph, 0xFF0u);
 constexpr uint32_t kProgB16 = prog_encode(1, kProgB16Ph, 0xF00u);
 constexpr uint32_t kProgB16x = prog_encode(3, kProgB16xPh, 0xF0Fu);
+// Balanced two-layout schedule (n = 20): the column group's Ry of stage s is
+// applied by the pass that applies D_s, so both layouts run round 0 on their 8
+// row qubits and round 1 on rows + columns (4 phases, 20 Ry each).
+constexpr PassPhase kProgAltPh[4] = {{1, 1}, {2, 7}, {1, 4}, {0, 4}};
+constexpr uint32_t kProgAlt = prog_encode(4, kProgAltPh, 0xFFFu);
 
 struct PassParams {
     int n;

@@ -392,6 +392,7 @@ cudaError_t ensure_attrs() {
         if (e == cudaSuccess) e = set_smem(pass_bwd_dual<kProgB20>, dual_smem());
         if (e == cudaSuccess) e = set_smem(pass_bwd_dual<kProgB16>, dual_smem());
         if (e == cudaSuccess) e = set_smem(pass_bwd_dual<kProgB16x>, dual_smem());
+        if (e == cudaSuccess) e = set_smem(pass_bwd_dual<kProgAlt>, dual_smem());
         return e;
     });
 }
@@ -443,7 +444,9 @@ cudaError_t launch_pass(cudaStream_t st, bool backward, int grid, const PassPara
     const CUtensorMap &l = lam ? *lam : *psi_out;
     // straight-line kernels for the compiled programs (Z is measured at stage 0 only:
     // those passes take the runtime-dispatch kernel)
-    const uint32_t prog = progs_enabled() && !(backward && p.zmask) ? p.prog : 0u;
+    uint32_t prog = progs_enabled() && !(backward && p.zmask) ? p.prog : 0u;
+    static const bool ablate_alt = getenv("QF_ABLATE_ALT") && atoi(getenv("QF_ABLATE_ALT"));
+    if (ablate_alt && backward && (prog == kProgA || prog == kProgB20)) prog = kProgAlt; // timing only
     if (!backward) {
         const size_t sm = pass_smem(false, 2);
         if (prog == kProgA) pass_kernel<false, 2, kProgA><<<grid, kThreads, sm, st>>>(p, *psi_in, *psi_out, l);
@@ -459,6 +462,7 @@ cudaError_t launch_pass(cudaStream_t st, bool backward, int grid, const PassPara
         else if (prog == kProgB20) pass_bwd_dual<kProgB20><<<grid, kDualThreads, sm, st>>>(p, *psi_in, *psi_out, l);
         else if (prog == kProgB16) pass_bwd_dual<kProgB16><<<grid, kDualThreads, sm, st>>>(p, *psi_in, *psi_out, l);
         else if (prog == kProgB16x) pass_bwd_dual<kProgB16x><<<grid, kDualThreads, sm, st>>>(p, *psi_in, *psi_out, l);
+        else if (prog == kProgAlt) pass_bwd_dual<kProgAlt><<<grid, kDualThreads, sm, st>>>(p, *psi_in, *psi_out, l);
         else pass_bwd_dual<0><<<grid, kDualThreads, sm, st>>>(p, *psi_in, *psi_out, l);
     } else {
         pass_kernel<true, 1><<<grid, kThreads, pass_smem(true, 1), st>>>(p, *psi_in, *psi_out, l);

@@ -116,7 +116,11 @@ __device__ __forceinline__ void wdiag(float2 (&v)[64], float2 base, unsigned lon
         const uint32_t flip = uint32_t(sgn >> j) << 31;
         g.x = __uint_as_float(__float_as_uint(g.x) ^ flip);
         g.y = __uint_as_float(__float_as_uint(g.y) ^ flip);
+#if QF_DIAG2
+        v[j] = cmul_p(g, v[j]);
+#else
         v[j] = cmul(g, v[j]);
+#endif
     }
 }
 

@@ -7,6 +7,8 @@
 //
 // Observable (engine.cpp:346-435): lambda = 2 O' psi, E_s = <psi|O'|psi>,
 // with the circuit's final diagonal folded in, O' = D_f^dag O D_f.
+// scalar complex products in the diagonal (packed FMUL2/FFMA2 measured -0.3% here)
+#define QF_DIAG2 0
 #include "qf_device.cuh"
 
 namespace qfb {
