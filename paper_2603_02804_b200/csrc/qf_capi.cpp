@@ -189,6 +189,12 @@ struct qf_plan {
     std::vector<size_t> tileinfo_off; // [czset * layouts + layout]
     CzAdj *final_adj = nullptr;
     int *stage_cz = nullptr, *stage_layout = nullptr, *dq = nullptr;
+    // balanced backward (P.alt): diagonal tables of layout A in the group-2 view
+    DiagTab *dtab_alt = nullptr;
+    CzTab *cztab_alt = nullptr;
+    uint32_t *tileinfo_alt = nullptr;
+    std::vector<size_t> tileinfo_alt_off; // [czset]
+    int *dq_alt = nullptr;                // [A with gd = 2, B][28]
     uint32_t *sec_q = nullptr, *sec_stage = nullptr, *sec_alpha = nullptr, *sec_off = nullptr,
              *sec_gates = nullptr;
     double *kpart = nullptr, *kout = nullptr, *epart = nullptr;
@@ -355,6 +361,19 @@ void build_device_plan(qf_plan *pl) {
     std::vector<int> dq;
     for (const PassLayout &L : P.layouts) dq.insert(dq.end(), L.dq, L.dq + 28);
     pl->dq = dupload(dq, o);
+    if (P.alt) {
+        pl->dtab_alt = dalloc<DiagTab>(std::max<uint32_t>(S, 1), o);
+        if (!P.cztab_alt.empty()) pl->cztab_alt = dupload(P.cztab_alt, o);
+        std::vector<uint32_t> ta;
+        for (const auto &t : P.tileinfo_alt) {
+            pl->tileinfo_alt_off.push_back(ta.size());
+            ta.insert(ta.end(), t.begin(), t.end());
+        }
+        if (!ta.empty()) pl->tileinfo_alt = dupload(ta, o);
+        std::vector<int> dqa(P.dq_alt, P.dq_alt + 28);
+        dqa.insert(dqa.end(), P.layouts[1].dq, P.layouts[1].dq + 28);
+        pl->dq_alt = dupload(dqa, o);
+    }
     pl->sec_q = dupload(P.sec_q, o);
     pl->sec_stage = dupload(P.sec_stage, o);
     pl->sec_alpha = dupload(P.sec_alpha_row, o);
@@ -432,6 +451,10 @@ void enqueue_prep(qf_plan *pl, const double *theta_dev, qf_stats &st) {
         ck(launch_diag_tables(s, int(P.stages), int(P.n), pl->wg, pl->wa, pl->stage_layout, pl->dq,
                               pl->dtab, pl->wfinal),
            "diag_tables");
+        if (P.alt)
+            ck(launch_diag_tables(s, int(P.stages), int(P.n), pl->wg, pl->wa, pl->stage_layout, pl->dq_alt,
+                                  pl->dtab_alt, pl->wfinal),
+               "diag_tables (balanced backward)");
         if (P.wide)
             ck(launch_diag_tables_wide(s, int(P.stages), int(P.n), pl->wg, pl->wa, pl->stage_layout, pl->dqw,
                                        pl->dtabw),
@@ -440,7 +463,7 @@ void enqueue_prep(qf_plan *pl, const double *theta_dev, qf_stats &st) {
     st.kernel_launches += 2;
 }
 
-PassParams pass_params(qf_plan *pl, const PassStep &ps, bool write_psi) {
+PassParams pass_params(qf_plan *pl, const PassStep &ps, bool write_psi, bool balanced = false) {
     const Plan &P = pl->P;
     const PassLayout &L = P.layouts[ps.layout];
     PassParams p{};
@@ -448,7 +471,9 @@ PassParams pass_params(qf_plan *pl, const PassStep &ps, bool write_psi) {
     p.tiles = int(uint64_t(P.batch) << (P.n - 12));
     p.tile_lo_bits = L.tile_lo_bits;
     p.tile_hi_bits = L.tile_hi_bits;
-    p.rot_mask = L.rot_mask;
+    p.rot0 = ps.rot0 | ps.rot1 ? ps.rot0 : L.rot_mask;
+    p.rot1 = ps.rot0 | ps.rot1 ? ps.rot1 : L.rot_mask;
+    p.rot_mask = p.rot0 | p.rot1;
     for (int l = 0; l < 12; ++l) p.qmap[l] = L.qmap[l];
     p.s0 = ps.s0;
     p.s1 = ps.s1;
@@ -456,13 +481,24 @@ PassParams pass_params(qf_plan *pl, const PassStep &ps, bool write_psi) {
     for (int i = 0; i < ps.nph; ++i) p.ph[i] = ps.ph[i];
     p.gd = L.gd;
     p.ry = pl->ry;
-    if (ps.sd >= 0) {
+    if (ps.sd >= 0 && balanced) { // layout A with the diagonal in group 2; layout B as is
+        p.gd = 2;
+        p.dt = pl->dtab_alt + ps.sd;
+        const int c = P.stage_cz[ps.sd];
+        if (c >= 0 && ps.layout == 0) {
+            p.cz = pl->cztab_alt + c;
+            p.tileinfo = pl->tileinfo_alt + pl->tileinfo_alt_off[c];
+        } else if (c >= 0) {
+            p.cz = pl->cztab + size_t(c) * P.layouts.size() + ps.layout;
+            p.tileinfo = pl->tinfo(c, ps.layout);
+        }
+    } else if (ps.sd >= 0) {
         p.dt = pl->dtab + ps.sd;
         const int c = P.stage_cz[ps.sd];
         p.cz = c >= 0 ? pl->cztab + size_t(c) * P.layouts.size() + ps.layout : nullptr;
         p.tileinfo = c >= 0 ? pl->tinfo(c, ps.layout) : nullptr;
     }
-    if (P.wide && ps.layout == 0 && ps.sd >= 0) {
+    if (P.wide && ps.layout == 0 && ps.sd >= 0 && !balanced) {
         p.dtw = pl->dtabw + ps.sd;
         const int c = P.stage_cz[ps.sd];
         p.czw = c >= 0 ? pl->cztabw + c : nullptr;
@@ -535,16 +571,16 @@ void enqueue_fused(qf_plan *pl, const double *theta_dev, double *out_dev, qf_sta
         const float2 *final_state = !NPS ? pl->psi0_src
                                     : ms  ? pl->W
                                           : pl->slots + size_t(P.n_slots - 1) * pl->amps_padded;
-        auto slot16 = [&](size_t pi) { return pl->slots16 + size_t(pi / P.ckpt_passes) * pl->amps_padded; };
+        auto slot16 = [&](size_t pi) { return pl->slots16 + P.slot_index(pi) * pl->amps_padded; };
         // forward (MemSave: every pass in place on W; a slot pass is narrowed into its bf16 slot)
         std::unique_ptr<Nvtx> range(new Nvtx("qfuse forward"));
         for (size_t pi = 0; pi < NPS; ++pi) {
             const PassStep &ps = P.steps[pi];
             const CUtensorMap *in;
             if (pi == 0) in = &pl->m_psi0[ps.layout];
-            else if (!ms && P.slot_pass(pi - 1)) in = &pl->m_slot[(pi - 1) / P.ckpt_passes][ps.layout];
+            else if (!ms && P.slot_pass(pi - 1)) in = &pl->m_slot[P.slot_index(pi - 1)][ps.layout];
             else in = &pl->m_W[ps.layout];
-            const CUtensorMap *outm = (!ms && P.slot_pass(pi)) ? &pl->m_slot[pi / P.ckpt_passes][ps.layout]
+            const CUtensorMap *outm = (!ms && P.slot_pass(pi)) ? &pl->m_slot[P.slot_index(pi)][ps.layout]
                                                                : &pl->m_W[ps.layout];
             PassParams p = pass_params(pl, ps, true);
             const int grid = pass_is_wide(false, p) ? std::min(wide_grid(pl->ctx->sms), p.tiles)
@@ -581,9 +617,9 @@ void enqueue_fused(qf_plan *pl, const double *theta_dev, double *out_dev, qf_sta
         range.reset(new Nvtx("qfuse backward"));
         if (!forward_only) {
             for (size_t pi = NPS; pi-- > 0;) {
-                const PassStep &ps = P.steps[pi];
+                const PassStep &ps = P.bstep(pi);
                 const bool from_slot = P.slot_pass(pi);
-                const CUtensorMap *in = (from_slot && !ms) ? &pl->m_slot[pi / P.ckpt_passes][ps.layout]
+                const CUtensorMap *in = (from_slot && !ms) ? &pl->m_slot[P.slot_index(pi)][ps.layout]
                                                            : &pl->m_W[ps.layout];
                 if (ms && from_slot && pi + 1 < NPS) { // re-anchor from the bf16 slot
                     // (W is free: the pass after a slot pass did not write psi)
@@ -592,7 +628,7 @@ void enqueue_fused(qf_plan *pl, const double *theta_dev, double *out_dev, qf_sta
                     bytes += 1.5 * sb;
                 }
                 const bool write_psi = pi > 0 && !P.slot_pass(pi - 1);
-                PassParams p = pass_params(pl, ps, write_psi);
+                PassParams p = pass_params(pl, ps, write_psi, P.alt);
                 pl->timed(1, (write_psi ? 4 : 3) * sb, [&] {
                     ck(launch_pass(s, true, pl->grid_bwd, p, in, &pl->m_W[ps.layout], &pl->m_lam[ps.layout]),
                        "pass bwd");

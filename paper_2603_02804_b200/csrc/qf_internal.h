@@ -116,7 +116,8 @@ struct PassParams {
     int tiles;
     int tile_lo_bits;  // tile bits between the column and the rows (row_start - 4)
     int tile_hi_bits;  // tile bits above the rows (n - row_start - 8)
-    uint32_t rot_mask; // local bits rotated by this layout
+    uint32_t rot_mask; // local bits rotated by this pass (rot0 | rot1)
+    uint32_t rot0, rot1; // ... in round 0 / round 1 (they differ in the balanced backward)
     int qmap[12];      // local bit -> qubit
     int s0, s1;        // stages of rounds 0 / 1 (-1 = absent)
     int nph;

@@ -33,7 +33,7 @@ __device__ bool pass_prologue(const PassParams &p, uint32_t tid, float4 *rys, fl
         const int r = tid / 12, lb = tid % 12;
         const int s = r == 0 ? p.s0 : p.s1;
         float4 v = make_float4(0.f, 0.f, 1.f, 0.f); // identity: t = 0, m = 1
-        if (s >= 0 && ((p.rot_mask >> lb) & 1u)) v = ry_entry(p.ry[size_t(s) * p.n + p.qmap[lb]]);
+        if (s >= 0 && (((r == 0 ? p.rot0 : p.rot1) >> lb) & 1u)) v = ry_entry(p.ry[size_t(s) * p.n + p.qmap[lb]]);
         rys[tid] = v;
     } else if (tid >= 40 && tid < 46) { // product of the factored m per (round, group)
         const int r = (tid - 40) / 3, g = (tid - 40) % 3;
@@ -41,7 +41,7 @@ __device__ bool pass_prologue(const PassParams &p, uint32_t tid, float4 *rys, fl
         float M = 1.f;
         for (int b = 0; b < 4; ++b) {
             const int lb = 4 * g + b;
-            if (s >= 0 && ((p.rot_mask >> lb) & 1u)) M *= ry_entry(p.ry[size_t(s) * p.n + p.qmap[lb]]).z;
+            if (s >= 0 && (((r == 0 ? p.rot0 : p.rot1) >> lb) & 1u)) M *= ry_entry(p.ry[size_t(s) * p.n + p.qmap[lb]]).z;
         }
         mgs[tid - 40] = make_float2(M, M);
     }
@@ -178,7 +178,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks(BWD, NB))
         if (tid < 2 * 12 * 8) {
             const int r = tid / 96, lb = (tid / 8) % 12, c = tid & 7;
             const int s = r == 0 ? p.s0 : p.s1;
-            if (s >= 0 && ((p.rot_mask >> lb) & 1u)) {
+            if (s >= 0 && (((r == 0 ? p.rot0 : p.rot1) >> lb) & 1u)) {
                 double sum = 0.0;
 #pragma unroll
                 for (int w = 0; w < 8; ++w) sum += acc[((w * 2 + r) * 12 + lb) * 8 + c];
@@ -278,7 +278,7 @@ __global__ void __launch_bounds__(kDualThreads, 1)
             r += __shfl_xor_sync(0xffffffffu, r, 8);
             r += __shfl_xor_sync(0xffffffffu, r, 16);
             const int rr = i / 3, g = i % 3, bit = int(lane >> 1), comp = int(lane & 1u);
-            if (lane < 8 && ((p.rot_mask >> (4 * g + bit)) & 1u))
+            if (lane < 8 && (((rr == 0 ? p.rot0 : p.rot1) >> (4 * g + bit)) & 1u))
                 acc[((warp * 2 + rr) * 12 + 4 * g + bit) * 8 + comp] += double(r);
             kreg[i] = 0.f;
         }
@@ -352,7 +352,7 @@ __global__ void __launch_bounds__(kDualThreads, 1)
     if (tid < 2 * 12 * 8) {
         const int r = tid / 96, lb = (tid / 8) % 12, c = tid & 7;
         const int s = r == 0 ? p.s0 : p.s1;
-        if (s >= 0 && ((p.rot_mask >> lb) & 1u)) {
+        if (s >= 0 && (((r == 0 ? p.rot0 : p.rot1) >> lb) & 1u)) {
             double sum = 0.0;
 #pragma unroll
             for (int w = 0; w < 16; ++w) sum += acc[((w * 2 + r) * 12 + lb) * 8 + c];

@@ -17,6 +17,7 @@
 #include "qf_plan.h"
 
 #include <algorithm>
+#include <cstdlib>
 #include <map>
 
 namespace qfb {
@@ -239,39 +240,43 @@ Plan make_plan(const qf_gate *gates, size_t n_gates, uint32_t n, uint32_t n_para
     const int NL = static_cast<int>(plan.layouts.size());
 
     // ---- CZ sign tables per (CZ set, layout)
+    auto cz_tables = [&](const std::vector<uint32_t> &adj, const PassLayout &L, CzTab &ct,
+                         std::vector<uint32_t> &ti) {
+        auto qset = [&](const int *qs, int k, uint32_t v) { // Q of the set bits
+            uint32_t par = 0;
+            for (int i = 0; i < k; ++i) {
+                if (!((v >> i) & 1u) || qs[i] < 0) continue;
+                for (int j = i + 1; j < k; ++j)
+                    if (((v >> j) & 1u) && qs[j] >= 0) par ^= (adj[qs[i]] >> qs[j]) & 1u;
+            }
+            return par;
+        };
+        auto cross = [&](const int *qs, int k, uint32_t v, const int *to, int kto) {
+            uint32_t m = 0;
+            for (int i = 0; i < k; ++i) {
+                if (!((v >> i) & 1u) || qs[i] < 0) continue;
+                for (int r = 0; r < kto; ++r)
+                    if (to[r] >= 0) m ^= ((adj[qs[i]] >> to[r]) & 1u) << r;
+            }
+            return m;
+        };
+        const int *reg = L.dq, *thr = L.dq + 4;
+        ct = CzTab{};
+        for (uint32_t j = 0; j < 16; ++j) ct.qreg |= qset(reg, 4, j) << j;
+        for (uint32_t tau = 0; tau < 256; ++tau)
+            ct.thrinfo[tau] = static_cast<uint16_t>((qset(thr, 8, tau) << 4) | cross(thr, 8, tau, reg, 4));
+        const int kt = static_cast<int>(L.tile_qubits.size());
+        ti.assign(size_t(1) << kt, 0u);
+        for (uint32_t tb = 0; tb < ti.size(); ++tb)
+            ti[tb] = qset(L.tile_qubits.data(), kt, tb) | (cross(L.tile_qubits.data(), kt, tb, reg, 4) << 1) |
+                     (cross(L.tile_qubits.data(), kt, tb, thr, 8) << 8);
+    };
     for (size_t c = 0; c < adjs.size(); ++c) {
-        const auto &adj = adjs[c];
         for (int li = 0; li < NL; ++li) {
-            const PassLayout &L = plan.layouts[li];
-            auto qset = [&](const int *qs, int k, uint32_t v) { // Q of the set bits
-                uint32_t par = 0;
-                for (int i = 0; i < k; ++i) {
-                    if (!((v >> i) & 1u) || qs[i] < 0) continue;
-                    for (int j = i + 1; j < k; ++j)
-                        if (((v >> j) & 1u) && qs[j] >= 0) par ^= (adj[qs[i]] >> qs[j]) & 1u;
-                }
-                return par;
-            };
-            auto cross = [&](const int *qs, int k, uint32_t v, const int *to, int kto) {
-                uint32_t m = 0;
-                for (int i = 0; i < k; ++i) {
-                    if (!((v >> i) & 1u) || qs[i] < 0) continue;
-                    for (int r = 0; r < kto; ++r)
-                        if (to[r] >= 0) m ^= ((adj[qs[i]] >> to[r]) & 1u) << r;
-                }
-                return m;
-            };
-            const int *reg = L.dq, *thr = L.dq + 4;
-            CzTab ct{};
-            for (uint32_t j = 0; j < 16; ++j) ct.qreg |= qset(reg, 4, j) << j;
-            for (uint32_t tau = 0; tau < 256; ++tau)
-                ct.thrinfo[tau] = static_cast<uint16_t>((qset(thr, 8, tau) << 4) | cross(thr, 8, tau, reg, 4));
+            CzTab ct;
+            std::vector<uint32_t> ti;
+            cz_tables(adjs[c], plan.layouts[li], ct, ti);
             plan.cztab.push_back(ct);
-            const int kt = static_cast<int>(L.tile_qubits.size());
-            std::vector<uint32_t> ti(size_t(1) << kt);
-            for (uint32_t tb = 0; tb < ti.size(); ++tb)
-                ti[tb] = qset(L.tile_qubits.data(), kt, tb) | (cross(L.tile_qubits.data(), kt, tb, reg, 4) << 1) |
-                         (cross(L.tile_qubits.data(), kt, tb, thr, 8) << 8);
             plan.tileinfo.push_back(std::move(ti));
         }
     }
@@ -391,7 +396,52 @@ Plan make_plan(const qf_gate *gates, size_t n_gates, uint32_t n, uint32_t n_para
         const uint32_t pps = static_cast<uint32_t>(std::max(1, NL - 1));
         plan.ckpt_passes = k * pps;
         const size_t np = plan.steps.size();
-        plan.n_slots = np == 0 ? 0 : static_cast<uint32_t>((np + plan.ckpt_passes - 1) / plan.ckpt_passes);
+        // balanced backward (Plan::alt): n = 20 with layouts A (12 rotated) and B (rows
+        // 12..19), strict A/B alternation with pass p applying D_p, an even slot period
+        const char *ea = getenv("QF_ALT");
+        bool alt = (!ea || atoi(ea) != 0) && n == 20 && NL == 2 && plan.layouts[0].rot_mask == 0xFFFu &&
+                   plan.layouts[0].gd == 0 && plan.layouts[1].rot_mask == 0xFF0u && plan.layouts[1].gd == 2 &&
+                   plan.ckpt_passes % 2 == 0 && np >= 2;
+        for (size_t pi = 0; alt && pi < np; ++pi) {
+            const PassStep &ps = plan.steps[pi];
+            const int p = static_cast<int>(pi);
+            if (pi + 1 < np)
+                alt = ps.layout == p % 2 && ps.sd == p && ps.s1 == p && ps.s0 == p - 1;
+            else
+                alt = ps.layout == p % 2 && ps.sd < 0 && ps.s1 < 0 && ps.s0 == p - 1 && p == S;
+        }
+        if (alt) {
+            plan.alt = true;
+            plan.slot_off = 1;
+            PassLayout LA = plan.layouts[0];
+            LA.gd = 2;
+            finish_layout(LA);
+            for (int i = 0; i < 28; ++i) plan.dq_alt[i] = LA.dq[i];
+            for (size_t c = 0; c < adjs.size(); ++c) {
+                CzTab ct;
+                std::vector<uint32_t> ti;
+                cz_tables(adjs[c], LA, ct, ti);
+                plan.cztab_alt.push_back(ct);
+                plan.tileinfo_alt.push_back(std::move(ti));
+            }
+            for (const PassStep &ps : plan.steps) {
+                // round 0: the layout's 8 row qubits; D; round 1: rows + columns
+                PassStep b = ps;
+                b.rot0 = ps.s0 >= 0 ? 0xFF0u : 0u;
+                b.rot1 = ps.s1 >= 0 ? 0xFFFu : 0u;
+                b.nph = 0;
+                auto add = [&](int g, uint8_t ops) { b.ph[b.nph++] = PassPhase{int8_t(g), ops}; };
+                const uint8_t gd_ops = uint8_t((ps.s0 >= 0 ? 1 : 0) | (ps.sd >= 0 ? 2 : 0) | (ps.s1 >= 0 ? 4 : 0));
+                if (ps.s0 >= 0) add(1, 1);
+                add(2, gd_ops);
+                if (ps.s1 >= 0) {
+                    add(1, 4);
+                    add(0, 4);
+                }
+                plan.bsteps.push_back(b);
+            }
+        }
+        plan.n_slots = np == 0 ? 0 : static_cast<uint32_t>((np - 1 + plan.slot_off) / plan.ckpt_passes + 1);
     }
     return plan;
 }

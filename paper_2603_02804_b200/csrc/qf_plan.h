@@ -37,6 +37,7 @@ struct PassStep {
     int s0 = -1, s1 = -1, sd = -1;
     int nph = 0;
     PassPhase ph[6] = {};
+    uint32_t rot0 = 0, rot1 = 0; // local bits rotated in round 0 / 1 (0, 0: the layout's rot_mask)
 };
 
 struct Plan {
@@ -64,6 +65,17 @@ struct Plan {
     int dqw[28] = {};
     std::vector<CzTabW> cztabw;                   // [czset]
     std::vector<std::vector<uint32_t>> tileinfow; // [czset]
+    // Balanced backward (n = 20): the column group's Ry of stage s is
+    // undone by the backward pass that undoes D_s, so both layouts' backward passes
+    // rotate 8 + 12 qubits (kProgAlt, 4 phases each) instead of 24 / 16. The forward
+    // keeps `steps`; both schedules pass through the same state after every layout-A
+    // pass, where the checkpoint slots sit (slot_off = 1).
+    bool alt = false;
+    std::vector<PassStep> bsteps;               // backward passes (alt), same indices as steps
+    std::vector<CzTab> cztab_alt;               // [czset] layout A, diagonal in group 2
+    std::vector<std::vector<uint32_t>> tileinfo_alt; // [czset]
+    int dq_alt[28] = {};                        // diag view of layout A with gd = 2
+    uint32_t slot_off = 0;
     uint32_t ckpt_stages = 1;      // k in stages
     uint32_t ckpt_layers = 0;      // k in layers as reported
     uint32_t ckpt_passes = 1;      // k in passes (streaming)
@@ -71,8 +83,10 @@ struct Plan {
     std::vector<qf_gate> gates;    // as given (per-gate comparator)
 
     bool slot_pass(size_t p) const {
-        return (p + 1) % ckpt_passes == 0 || p + 1 == steps.size();
+        return (p + 1 + slot_off) % ckpt_passes == 0 || p + 1 == steps.size();
     }
+    size_t slot_index(size_t p) const { return (p + slot_off) / ckpt_passes; }
+    const PassStep &bstep(size_t p) const { return alt ? bsteps[p] : steps[p]; }
 };
 
 Plan make_plan(const qf_gate *gates, size_t n_gates, uint32_t n_qubits, uint32_t n_params,

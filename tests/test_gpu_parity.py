@@ -701,3 +701,40 @@ def test_hea_17_19_deep_vs_oracle(ctx, oracle, n):
     gates, npar, theta, psi0, pauli = _hea_case(n, 20, 1, seed=300 + n)
     res = capi.gradient_c64(ctx, gates, n, npar, 20, 10, psi0, theta, pauli)
     _check(res, oracle.gradient(gates, n, npar, psi0, theta, pauli))
+
+
+# ---- balanced backward at n = 20 (Plan::alt, qf_plan.cpp / DESIGN.md §4): the
+# column group's Ry undone by the pass that undoes D_s, slots after layout-A passes
+@pytest.mark.parametrize("layers,k,batch,storage", [
+    (6, 2, 2, "full"),      # balanced (even slot period)
+    (9, 3, 1, "full"),      # odd slot period: plain backward
+    (10, 2, 1, "memsave"),  # balanced + bf16 slots
+    (7, 0, 1, "full"),      # default k (min(stages, 10) = 7: odd)
+    (4, 4, 2, "full"),      # one slot block
+])
+def test_balanced_backward_20q(ctx, oracle, layers, k, batch, storage):
+    n = 20
+    gates, npar, theta, psi0, pauli = _hea_case(n, layers, batch, seed=900 + layers)
+    res = capi.gradient_c64(ctx, gates, n, npar, layers, k, psi0, theta, pauli, storage=storage)
+    ref = oracle.gradient(gates, n, npar, psi0, theta, pauli)
+    if storage == "memsave":
+        assert rel_diff(res.gradient, ref[1]) <= MEMSAVE_TOL
+    else:
+        _check(res, ref)
+
+
+def test_balanced_backward_matches_plain(ctx, monkeypatch):
+    """The balanced and the plain backward schedules (QF_ALT=0) are the same
+    gradient up to fp32 rounding (20q x 40 layers, k = 10)."""
+    n, layers = 20, 40
+    gates, npar, theta, psi0, pauli = _hea_case(n, layers, 2, seed=31)
+
+    def run():  # a fresh plan: QF_ALT is read by the planner
+        plan = capi.Plan(ctx, gates, n, npar, layers, 10, 2, pauli)
+        plan.upload_psi0(psi0)
+        return plan.gradient(theta)
+    a = run()
+    monkeypatch.setenv("QF_ALT", "0")
+    b = run()
+    assert rel_diff(a.gradient, b.gradient) <= 1e-5
+    assert rel_diff(a.expect, b.expect) == 0.0  # same forward schedule
