@@ -9,21 +9,28 @@
 // CZ run = one diagonal sign (apply_cz_kernel engine.cpp:111-136); a CNOT =
 // a conditional pair swap (apply_cnot_kernel engine.cpp:142-170). A segment is
 // a range of ops whose non-diagonal targets fit one tile of 2^m amplitudes in
-// shared memory (m = min(n, 10); qubits 0..2 always local so every 8
-// amplitudes are one 128-B line). One CTA loads a tile (psi, and lambda in
-// the backward), runs the segment's ops on it between __syncthreads, and
-// writes it back.
+// shared memory (m = min(n, 11); qubits 0..2 always local so every 8
+// amplitudes are one 128-B line): one HBM pass. One CTA loads a tile (psi, and
+// lambda in the backward) and runs the segment's *rounds* on it: a round holds
+// up to three sections on (at most) three local bits plus the CZ runs between
+// them, applied to the eight amplitudes of those bits in each thread's
+// registers (one shared-memory read and write per round); a CNOT is a round of
+// its own (pair swaps in shared memory).
 //
 // Backward: for each section, in reverse, psi_in = U^dag psi_out and lam_in =
 // U^dag lam_out (psi uncomputed in place: unitary in fp64, the same choice as
-// the per-gate c128 path), and K = sum_pairs psi_in lam_in^dag (2x2) is
-// accumulated. The gradient of rotation j of the section is
-//   Re <lam_out| A_j dg_j B_j |psi_in> = Re Tr(M_j K),  M_j = B_j^dag g_j^dag dg_j B_j
-// (B_j = the rotations before j, A_j after; rotation_derivative
-// circuit.cpp:76-87), evaluated in fp64 by c128_finalize. K partials are
-// reduced per warp (reduce-scatter), per CTA in fixed warp order, and over
-// CTAs in fixed order by the last CTA of the segment: deterministic.
+// the per-gate c128 path). The gradient of rotation j of the section is
+//   Re <lam_out| A_j dg_j B_j |psi_in> = Re Tr(M_j K),  K = sum_pairs psi_in lam_in^dag,
+// M_j = B_j^dag g_j^dag dg_j B_j (B_j = the rotations before j; rotation_derivative
+// circuit.cpp:76-87). With dg = -(i/2) P g, M_j = -(i/2) H_j, H_j = sum_m h_m sigma_m
+// hermitian and traceless, so Re Tr(M_j K) = (1/2)(hx X + hy Y + hz Z) with
+//   X = Im(K01 + K10), Y = Re(K01 - K10), Z = Im(K00 - K11):
+// three accumulators per section (12 FMA per pair instead of 16), evaluated in
+// fp64 by c128_finalize. K partials are reduced per warp, per CTA in fixed warp
+// order, and over CTAs in fixed order by the last CTA of the segment:
+// deterministic.
 #include <algorithm>
+#include <functional>
 #include <set>
 #include <stdexcept>
 
@@ -76,34 +83,37 @@ __global__ void c128_prep(int nsec, const uint32_t *off, const uint32_t *cnt, co
     secU[4 * s + 3] = U.d;
 }
 
-// K layout per section: K00, K01, K10, K11 as (re, im) = 8 doubles.
+// K per section: (X, Y, Z); grad of rotation j = (1/2)(hx X + hy Y + hz Z) with
+// H_j = B_j^dag g_j^dag P_j g_j B_j = [[hz, hx - i hy], [hx + i hy, -hz]].
 __global__ void c128_finalize(int nsec, const uint32_t *off, const uint32_t *cnt,
                               const uint32_t *gates, const double *theta, const double *K,
                               double *grad) {
     const int s = blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= nsec) return;
-    const double *k = K + size_t(s) * 8;
-    const Cx2 Kq = {make_double2(k[0], k[1]), make_double2(k[2], k[3]), make_double2(k[4], k[5]),
-                    make_double2(k[6], k[7])};
+    const double X = K[size_t(s) * 3 + 0], Y = K[size_t(s) * 3 + 1], Z = K[size_t(s) * 3 + 2];
     Cx2 B = ident();
     for (uint32_t i = 0; i < cnt[s]; ++i) {
         const uint32_t g = gates[off[s] + i];
         const int axis = int(g & 3u);
         double sn, cs;
         sincos(theta[g >> 2] / 2.0, &sn, &cs);
-        const Cx2 u = rot(axis, cs, sn), du = rot(axis, -0.5 * sn, 0.5 * cs);
-        const Cx2 M = mul(dag(B), mul(dag(u), mul(du, B)));
-        const Cx2 MK = mul(M, Kq);
-        grad[g >> 2] = MK.a.x + MK.d.x; // Re Tr(M K)
-        B = mul(u, B);
+        const Cx2 u = rot(axis, cs, sn), P = rot(axis, 0.0, 1.0); // rot(axis, 0, 1) = -i P
+        const Cx2 uB = mul(u, B);
+        const Cx2 H = mul(dag(uB), mul(P, uB)); // = -i B^dag g^dag P g B
+        // H holds -i H_j: hz = Re H_j00 = -Im H00, hx + i hy = H_j10 = i H10
+        const double hz = -H.a.y, hx = -H.c.y, hy = H.c.x;
+        grad[g >> 2] = 0.5 * (hx * X + hy * Y + hz * Z);
+        B = uB;
     }
 }
 
-// Shared-memory slot of tile amplitude l: the low 3 bits are XORed with 7 when
-// bit 3 is set, so the 8 lanes of a quarter-warp hit 8 distinct 16-B bank groups
-// for pair accesses on every local bit (bits 0..2 would otherwise be 2-way
-// conflicted) and for consecutive amplitudes.
-__device__ __forceinline__ uint32_t sw(uint32_t l) { return l ^ (((l >> 3) & 1u) * 7u); }
+// Shared-memory slot of tile amplitude l: the low 3 bits (the 16-B bank group of a
+// complex128) XORed with the fold of the higher 3-bit chunks, so a quarter-warp's
+// eight 16-B accesses are conflict-free whenever its threads vary local bits whose
+// positions are distinct mod 3 (the round planner prefers such octets).
+__device__ __forceinline__ uint32_t sw2(uint32_t l) {
+    return l ^ (((l >> 3) ^ (l >> 6) ^ (l >> 9)) & 7u);
+}
 
 __device__ __forceinline__ uint32_t insert0(uint32_t p, uint32_t pos) {
     return ((p >> pos) << (pos + 1)) | (p & ((1u << pos) - 1u));
@@ -119,58 +129,70 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 struct U2 { // a section's unitary, or its adjoint
     double2 u00, u01, u10, u11;
 };
-__device__ __forceinline__ U2 load_u(const double2 *secU, uint32_t s, bool adjoint) {
-    const double2 *u = secU + 4 * size_t(s);
+__device__ __forceinline__ U2 load_u(const double2 *u, bool adjoint) {
     const double2 a = u[0], b = u[1], c = u[2], d = u[3];
     return adjoint ? U2{cj(a), cj(c), cj(b), cj(d)} : U2{a, b, c, d};
 }
+// a' = u00 a + u01 b, b' = u10 a + u11 b: four independent FMA chains (one DMUL +
+// three DFMA per component, 16 FP64 instructions per pair)
+__device__ __forceinline__ double2 cmac2(double2 x, double2 a, double2 y, double2 b) {
+    return make_double2(fma(x.x, a.x, fma(-x.y, a.y, fma(y.x, b.x, -y.y * b.y))),
+                        fma(x.x, a.y, fma(x.y, a.x, fma(y.x, b.y, y.y * b.x))));
+}
 __device__ __forceinline__ void apply_u(const U2 &u, double2 &a, double2 &b) {
     const double2 a0 = a, b0 = b;
-    a = cadd(cm(u.u00, a0), cm(u.u01, b0));
-    b = cadd(cm(u.u10, a0), cm(u.u11, b0));
+    a = cmac2(u.u00, a0, u.u01, b0);
+    b = cmac2(u.u10, a0, u.u11, b0);
 }
-// K += [a; b] [la; lb]^dag (8 doubles: K00, K01, K10, K11 as re, im)
-__device__ __forceinline__ void kacc(double (&k8)[8], double2 a, double2 b, double2 la, double2 lb) {
-    const double2 k00 = cm(a, cj(la)), k01 = cm(a, cj(lb)), k10 = cm(b, cj(la)), k11 = cm(b, cj(lb));
-    k8[0] += k00.x; k8[1] += k00.y; k8[2] += k01.x; k8[3] += k01.y;
-    k8[4] += k10.x; k8[5] += k10.y; k8[6] += k11.x; k8[7] += k11.y;
+// section on register bit B of the 2^R amplitudes
+template <int B, int R> __device__ __forceinline__ void apply_bit(const U2 &u, double2 (&v)[1 << R]) {
+#pragma unroll
+    for (int j = 0; j < (1 << R); ++j)
+        if (!(j & (1 << B))) apply_u(u, v[j], v[j | (1 << B)]);
 }
-// Warp sum of the 8 values (reduce-scatter over 8-lane groups, then across the
-// groups), added by lanes 0..7 to this warp's accumulator slot.
-__device__ __forceinline__ void kflush(double (&k8)[8], uint32_t lane, double *slot) {
+// (X, Y, Z) of register bit B: X += Im(a lb* + b la*), Y += Re(a lb* - b la*),
+// Z += Im(a la* - b lb*)   (a, b = psi of the pair, la, lb = lambda)
+template <int B, int R>
+__device__ __forceinline__ void kacc_bit(double *k, const double2 (&v)[1 << R], const double2 (&w)[1 << R]) {
 #pragma unroll
-    for (int m = 4; m >= 1; m >>= 1) {
-        const bool up = (lane & uint32_t(m)) != 0;
-#pragma unroll
-        for (int i = 0; i < m; ++i) {
-            const double send = up ? k8[i] : k8[i + m];
-            const double keep = up ? k8[i + m] : k8[i];
-            k8[i] = keep + __shfl_xor_sync(0xffffffffu, send, m);
-        }
+    for (int j = 0; j < (1 << R); ++j) {
+        if (j & (1 << B)) continue;
+        const double2 a = v[j], b = v[j | (1 << B)], la = w[j], lb = w[j | (1 << B)];
+        k[0] = fma(a.y, lb.x, fma(-a.x, lb.y, fma(b.y, la.x, fma(-b.x, la.y, k[0]))));
+        k[1] = fma(a.x, lb.x, fma(a.y, lb.y, fma(-b.x, la.x, fma(-b.y, la.y, k[1]))));
+        k[2] = fma(a.y, la.x, fma(-a.x, la.y, fma(-b.y, lb.x, fma(b.x, lb.y, k[2]))));
     }
-    double v = k8[0];
-    v += __shfl_xor_sync(0xffffffffu, v, 8);
-    v += __shfl_xor_sync(0xffffffffu, v, 16);
-    if (lane < 8) slot[lane] += v;
 }
 
-template <bool BWD>
+constexpr int kWarps = kT / 32;
+// K slot s (runtime) -> accumulator row (compile-time indices: no local memory)
+template <int B, int R>
+__device__ __forceinline__ void kacc_slot(uint32_t slot, double (&kk)[kC128RoundSecs][3],
+                                          const double2 (&v)[1 << R], const double2 (&w)[1 << R]) {
+    if (slot == 0) kacc_bit<B, R>(kk[0], v, w);
+    else if (slot == 1) kacc_bit<B, R>(kk[1], v, w);
+    else kacc_bit<B, R>(kk[2], v, w);
+}
+
+template <bool BWD, int R>
 __global__ void __launch_bounds__(kT, 2) seg_c128(const C128Seg sg, const C128Op *__restrict__ ops,
+                                               const C128Round *__restrict__ rounds,
                                                const uint32_t *__restrict__ czp,
                                                const double2 *__restrict__ secU, double2 *psi,
                                                double2 *lam, int n, uint64_t tiles, double *kpart,
                                                unsigned *ticket, double *K) {
     extern __shared__ double2 sm[];
-    const uint32_t amps = 1u << sg.m, pairs = amps >> 1;
-    constexpr uint32_t kBufs = BWD ? 2u : 1u; // psi (+ lambda) per tile buffer
-    // two tile buffers: tile i+1 is copied in (cp.async) while tile i is processed
-    double *acc = reinterpret_cast<double *>(sm + 2 * kBufs * amps); // [sec][warp][8]
+    const uint32_t m = sg.m, amps = 1u << m;
+    double2 *sp = sm, *sl = sm + amps;
+    double *acc = reinterpret_cast<double *>(sm + (BWD ? 2u : 1u) * amps); // [sec][warp][3]
     const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31u;
-    // the segment's qubit maps, indexed at run time: shared copies (not a local
-    // copy of the parameter block)
     __shared__ int8_t lpos[32];
     __shared__ uint8_t lq[16], rq[32];
-    if (tid == 0) {
+    __shared__ C128Op ops_s[kC128MaxOps];
+    __shared__ C128Round rnd_s[kC128MaxRounds];
+    __shared__ double2 u_s[kC128MaxSec * 4];
+    __shared__ uint32_t cz_s[kC128MaxCzPairs];
+    if (tid == 0) { // constant indices: no local copy of the parameter block
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
             lpos[i] = sg.lpos[i];
@@ -178,188 +200,148 @@ __global__ void __launch_bounds__(kT, 2) seg_c128(const C128Seg sg, const C128Op
             if (i < 16) lq[i] = sg.lq[i];
         }
     }
-    // the segment's ops, section unitaries and CZ pairs, staged once per CTA
-    __shared__ C128Op ops_s[kC128MaxOps];
-    __shared__ double2 u_s[kC128MaxSec * 4];
-    __shared__ uint32_t cz_s[kC128MaxCzPairs];
-    const uint32_t nops = sg.op_end - sg.op_begin;
+    const uint32_t nops = sg.op_end - sg.op_begin, nrnd = sg.round_end - sg.round_begin;
     for (uint32_t i = tid; i < nops; i += kT) ops_s[i] = ops[sg.op_begin + i];
+    for (uint32_t i = tid; i < nrnd; i += kT) rnd_s[i] = rounds[sg.round_begin + i];
     for (uint32_t i = tid; i < sg.nsec * 4; i += kT) u_s[i] = secU[size_t(sg.sec_begin) * 4 + i];
     for (uint32_t i = tid; i < sg.cz_count; i += kT) cz_s[i] = czp[sg.cz_begin + i];
     if (BWD)
-        for (uint32_t i = tid; i < sg.nsec * 64; i += kT) acc[i] = 0.0;
+        for (uint32_t i = tid; i < sg.nsec * kWarps * 3; i += kT) acc[i] = 0.0;
     __syncthreads();
-    constexpr int KA = (1 << kC128TileBits) / kT; // amplitudes per thread
-    // local part of the global index of this thread's amplitudes (fixed per segment)
-    uint32_t xl[KA];
+    constexpr int KA = (1 << kC128TileBits) / kT; // tile amplitudes per thread (copy in / out)
+    // local part of their global index (recomputed at the copies: fewer live registers
+    // through the rounds)
+    uint32_t xla[KA];
 #pragma unroll
     for (int k = 0; k < KA; ++k) {
         const uint32_t l = tid + uint32_t(k) * kT;
         uint32_t x = 0;
-        for (uint32_t j = 0; j < sg.m; ++j) x |= ((l >> j) & 1u) << lq[j];
-        xl[k] = x;
+        for (uint32_t j = 0; j < m; ++j) x |= ((l >> j) & 1u) << lq[j];
+        xla[k] = x;
     }
-    // Q(xl) of every CZ run of the segment (op.q = its index < kC128MaxCz)
-    uint32_t qlb[KA];
-#pragma unroll
-    for (int k = 0; k < KA; ++k) qlb[k] = 0;
-    for (uint32_t i = 0; i < nops; ++i) {
-        const C128Op op = ops_s[i];
-        if (op.type != 1) continue;
-#pragma unroll
-        for (int k = 0; k < KA; ++k) {
-            uint32_t f = 0;
-            for (uint32_t c = 0; c < op.b; ++c) {
-                const uint32_t w = cz_s[op.a - sg.cz_begin + c];
-                f ^= (xl[k] >> (w & 255u)) & (xl[k] >> (w >> 8)) & 1u;
-            }
-            qlb[k] |= f << op.q;
-        }
-    }
+    auto xl = [&](int k) { return xla[k]; };
     auto tile_xr = [&](uint64_t t) {
         const uint32_t r = uint32_t(t) & ((1u << sg.nrest) - 1u);
         uint32_t xr = 0;
         for (uint32_t k = 0; k < sg.nrest; ++k) xr |= ((r >> k) & 1u) << rq[k];
         return xr;
     };
-    auto fetch = [&](uint64_t t, uint32_t buf) {
+    constexpr int NV = 1 << R;
+    for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
         const uint64_t base = (t >> sg.nrest) << n;
         const uint32_t xr = tile_xr(t);
-        double2 *dp = sm + buf * kBufs * amps;
 #pragma unroll
         for (int k = 0; k < KA; ++k) {
             const uint32_t l = tid + uint32_t(k) * kT;
             if (l < amps) {
-                cp_async16(dp + sw(l), psi + base + (xr | xl[k]));
-                if (BWD) cp_async16(dp + amps + sw(l), lam + base + (xr | xl[k]));
+                const uint32_t x = xr | xl(k);
+                cp_async16(sp + sw2(l), psi + base + x);
+                if (BWD) cp_async16(sl + sw2(l), lam + base + x);
             }
         }
         cp_async_commit();
-    };
-    uint32_t it = 0;
-    if (blockIdx.x < tiles) fetch(blockIdx.x, 0);
-    for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
-        const uint32_t buf = it & 1u;
-        double2 *sp = sm + buf * kBufs * amps, *sl = sp + amps;
-        const uint64_t base = (t >> sg.nrest) << n;
-        const uint32_t xr_cur = tile_xr(t);
-        uint32_t xs[KA];
-#pragma unroll
-        for (int k = 0; k < KA; ++k) xs[k] = xr_cur | xl[k];
         cp_async_wait_all();
         __syncthreads();
-        if (t + gridDim.x < tiles) fetch(t + gridDim.x, buf ^ 1u);
-        for (uint32_t ii = 0; ii < nops; ++ii) {
-            const C128Op op = ops_s[BWD ? nops - 1 - ii : ii];
-            if (op.type == 0 && ii + 1 < nops && amps >= 4) {
-                const C128Op op2 = ops_s[BWD ? nops - 2 - ii : ii + 1];
-                if (op2.type == 0 && op2.q != op.q) {
-                    // two sections on different qubits in one round: each thread
-                    // owns a quad (bits p1, p2) and applies (or undoes) op then op2
-                    // in registers; K of both is measured after both are undone
-                    // (K of a qubit is invariant under gates on other qubits)
-                    const uint32_t p1 = uint32_t(lpos[op.q]), p2 = uint32_t(lpos[op2.q]);
-                    const uint32_t lo = min(p1, p2), hi = max(p1, p2);
-                    const U2 ua = load_u(u_s, op.a - sg.sec_begin, BWD), ub = load_u(u_s, op2.a - sg.sec_begin, BWD);
-                    double ka[8] = {0, 0, 0, 0, 0, 0, 0, 0}, kb[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-                    if (tid < (amps >> 2)) { // amps / 4 <= kT: one quad per thread
-                        const uint32_t b0 = insert0(insert0(tid, lo), hi);
-                        uint32_t ix[2][2];
-                        double2 v[2][2], w[2][2];
-#pragma unroll
-                        for (int i = 0; i < 2; ++i)
-#pragma unroll
-                            for (int j = 0; j < 2; ++j) {
-                                ix[i][j] = sw(b0 | (uint32_t(i) << p1) | (uint32_t(j) << p2));
-                                v[i][j] = sp[ix[i][j]];
-                                if (BWD) w[i][j] = sl[ix[i][j]];
-                            }
-#pragma unroll
-                        for (int j = 0; j < 2; ++j) {
-                            apply_u(ua, v[0][j], v[1][j]);
-                            if (BWD) apply_u(ua, w[0][j], w[1][j]);
-                        }
-#pragma unroll
-                        for (int i = 0; i < 2; ++i) {
-                            apply_u(ub, v[i][0], v[i][1]);
-                            if (BWD) apply_u(ub, w[i][0], w[i][1]);
-                        }
-                        if (BWD) {
-#pragma unroll
-                            for (int j = 0; j < 2; ++j) kacc(ka, v[0][j], v[1][j], w[0][j], w[1][j]);
-#pragma unroll
-                            for (int i = 0; i < 2; ++i) kacc(kb, v[i][0], v[i][1], w[i][0], w[i][1]);
-                        }
-#pragma unroll
-                        for (int i = 0; i < 2; ++i)
-#pragma unroll
-                            for (int j = 0; j < 2; ++j) {
-                                sp[ix[i][j]] = v[i][j];
-                                if (BWD) sl[ix[i][j]] = w[i][j];
-                            }
-                    }
-                    if (BWD) {
-                        kflush(ka, lane, acc + ((op.a - sg.sec_begin) * 8 + warp) * 8);
-                        kflush(kb, lane, acc + ((op2.a - sg.sec_begin) * 8 + warp) * 8);
-                    }
-                    ++ii;
-                    __syncthreads();
-                    continue;
-                }
-            }
-            if (op.type == 0) { // a single section
-                const uint32_t pos = uint32_t(lpos[op.q]);
-                const U2 u = load_u(u_s, op.a - sg.sec_begin, BWD);
-                double k8[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-                for (uint32_t p = tid; p < pairs; p += kT) {
-                    const uint32_t i0 = sw(insert0(p, pos)), i1 = sw(insert0(p, pos) | (1u << pos));
-                    double2 a = sp[i0], b = sp[i1];
-                    apply_u(u, a, b);
-                    sp[i0] = a;
-                    sp[i1] = b;
-                    if (BWD) {
-                        double2 la = sl[i0], lb = sl[i1];
-                        apply_u(u, la, lb);
-                        sl[i0] = la;
-                        sl[i1] = lb;
-                        kacc(k8, a, b, la, lb);
-                    }
-                }
-                if (BWD) kflush(k8, lane, acc + ((op.a - sg.sec_begin) * 8 + warp) * 8);
-            } else if (op.type == 1) { // CZ run: one sign per amplitude
-                // Q(xr | xl) = Q(xr) ^ Q(xl) ^ parity(xl & M(xr)), M(xr) = the qubits
-                // with an odd number of CZ partners set in xr: the per-pair loop runs
-                // once per tile (warp-uniform) instead of once per amplitude, and
-                // Q(xl) of this thread's amplitudes is precomputed (qlb, bit op.q).
-                uint32_t qr = 0, M = 0;
-                for (uint32_t c = 0; c < op.b; ++c) {
-                    const uint32_t w = cz_s[op.a - sg.cz_begin + c], a = w & 255u, b = w >> 8;
-                    const uint32_t ra = (xr_cur >> a) & 1u, rb = (xr_cur >> b) & 1u;
-                    qr ^= ra & rb;
-                    M ^= (ra << b) ^ (rb << a);
-                }
-#pragma unroll
-                for (int k = 0; k < KA; ++k) {
-                    const uint32_t l = tid + uint32_t(k) * kT;
-                    if (l < amps && (qr ^ ((qlb[k] >> op.q) & 1u) ^ (__popc(xl[k] & M) & 1u))) {
-                        sp[sw(l)] = make_double2(-sp[sw(l)].x, -sp[sw(l)].y);
-                        if (BWD) sl[sw(l)] = make_double2(-sl[sw(l)].x, -sl[sw(l)].y);
-                    }
-                }
-            } else { // CNOT(control a, target q): self-inverse
+        for (uint32_t ri = 0; ri < nrnd; ++ri) {
+            const C128Round rd = rnd_s[BWD ? nrnd - 1 - ri : ri];
+            if (rd.kind == 1) { // CNOT(control a, target q): pair swaps, self-inverse
+                const C128Op op = ops_s[rd.op_begin - sg.op_begin];
                 const uint32_t pos = uint32_t(lpos[op.q]);
                 const int cpos = lpos[op.a];
-                for (uint32_t p = tid; p < pairs; p += kT) {
+                for (uint32_t p = tid; p < (amps >> 1); p += kT) {
                     const uint32_t i0 = insert0(p, pos), i1 = i0 | (1u << pos);
-                    const uint32_t ctl = cpos >= 0 ? (i0 >> cpos) & 1u : (xr_cur >> op.a) & 1u;
+                    const uint32_t ctl = cpos >= 0 ? (i0 >> cpos) & 1u : (xr >> op.a) & 1u;
                     if (ctl) {
-                        double2 tmp = sp[sw(i0)];
-                        sp[sw(i0)] = sp[sw(i1)];
-                        sp[sw(i1)] = tmp;
+                        double2 tmp = sp[sw2(i0)];
+                        sp[sw2(i0)] = sp[sw2(i1)];
+                        sp[sw2(i1)] = tmp;
                         if (BWD) {
-                            tmp = sl[sw(i0)];
-                            sl[sw(i0)] = sl[sw(i1)];
-                            sl[sw(i1)] = tmp;
+                            tmp = sl[sw2(i0)];
+                            sl[sw2(i0)] = sl[sw2(i1)];
+                            sl[sw2(i1)] = tmp;
+                        }
+                    }
+                }
+            } else {
+                double kk[kC128RoundSecs][3];
+#pragma unroll
+                for (int s2 = 0; s2 < kC128RoundSecs; ++s2) kk[s2][0] = kk[s2][1] = kk[s2][2] = 0.0;
+                if (tid < (amps >> R)) {
+                    uint32_t bl = tid; // local index of register offset 0
+#pragma unroll
+                    for (int i = 0; i < R; ++i) bl = insert0(bl, rd.bits[i]);
+                    // shared-memory slot of register offset j (recomputed at the store:
+                    // fewer live registers than keeping eight addresses)
+                    auto slot = [&](int j) {
+                        uint32_t o = 0;
+#pragma unroll
+                        for (int i = 0; i < R; ++i) o |= uint32_t((j >> i) & 1) << rd.bits[i];
+                        return sw2(bl | o);
+                    };
+                    double2 v[NV], w[NV];
+#pragma unroll
+                    for (int j = 0; j < NV; ++j) {
+                        const uint32_t a = slot(j);
+                        v[j] = sp[a];
+                        if (BWD) w[j] = sl[a];
+                    }
+                    uint32_t x0 = 0; // global index of register offset 0 (CZ runs only)
+                    if (rd.has_cz) {
+                        x0 = xr;
+                        for (uint32_t j = 0; j < m; ++j) x0 |= ((bl >> j) & 1u) << lq[j];
+                    }
+                    const uint32_t no = rd.op_end - rd.op_begin;
+                    for (uint32_t oi = 0; oi < no; ++oi) {
+                        const C128Op op = ops_s[(BWD ? rd.op_end - 1 - oi : rd.op_begin + oi) - sg.op_begin];
+                        if (op.type == 0) {
+                            const U2 u = load_u(u_s + (op.a - sg.sec_begin) * 4, BWD);
+                            if (op.q == 0) {
+                                apply_bit<0, R>(u, v);
+                                if (BWD) { apply_bit<0, R>(u, w); kacc_slot<0, R>(op.b, kk, v, w); }
+                            } else if (R > 1 && op.q == 1) {
+                                apply_bit<(R > 1 ? 1 : 0), R>(u, v);
+                                if (BWD) { apply_bit<(R > 1 ? 1 : 0), R>(u, w); kacc_slot<(R > 1 ? 1 : 0), R>(op.b, kk, v, w); }
+                            } else if (R > 2) {
+                                apply_bit<(R > 2 ? 2 : 0), R>(u, v);
+                                if (BWD) { apply_bit<(R > 2 ? 2 : 0), R>(u, w); kacc_slot<(R > 2 ? 2 : 0), R>(op.b, kk, v, w); }
+                            }
+                        } else { // CZ run: Q(x0 | o) = Q(x0) ^ Q(o) ^ parity(o & M(x0))
+                            uint32_t qx = 0, M = 0;
+                            for (uint32_t c = 0; c < op.b; ++c) {
+                                const uint32_t pr = cz_s[op.a - sg.cz_begin + c], a = pr & 255u, b = pr >> 8;
+                                const uint32_t ra = (x0 >> a) & 1u, rb = (x0 >> b) & 1u;
+                                qx ^= ra & rb;
+                                M ^= (ra << b) ^ (rb << a);
+                            }
+                            uint32_t mr = 0;
+#pragma unroll
+                            for (int i = 0; i < R; ++i) mr |= ((M >> rd.gq[i]) & 1u) << i;
+#pragma unroll
+                            for (int j = 0; j < NV; ++j) {
+                                if ((qx ^ (op.q >> j) ^ __popc(uint32_t(j) & mr)) & 1u) {
+                                    v[j] = make_double2(-v[j].x, -v[j].y);
+                                    if (BWD) w[j] = make_double2(-w[j].x, -w[j].y);
+                                }
+                            }
+                        }
+                    }
+#pragma unroll
+                    for (int j = 0; j < NV; ++j) {
+                        const uint32_t a = slot(j);
+                        sp[a] = v[j];
+                        if (BWD) sl[a] = w[j];
+                    }
+                }
+                if (BWD) { // warp sums of the round's (X, Y, Z), added to this warp's slots
+#pragma unroll
+                    for (uint32_t s2 = 0; s2 < uint32_t(kC128RoundSecs); ++s2) {
+                        if (s2 >= rd.nsec) break;
+#pragma unroll
+                        for (int c = 0; c < 3; ++c) {
+                            double x = kk[s2][c];
+#pragma unroll
+                            for (int o = 16; o >= 1; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+                            if (lane == 0) acc[(rd.sec[s2] * kWarps + warp) * 3 + c] += x;
                         }
                     }
                 }
@@ -370,18 +352,19 @@ __global__ void __launch_bounds__(kT, 2) seg_c128(const C128Seg sg, const C128Op
         for (int k = 0; k < KA; ++k) {
             const uint32_t l = tid + uint32_t(k) * kT;
             if (l < amps) {
-                psi[base + xs[k]] = sp[sw(l)];
-                if (BWD) lam[base + xs[k]] = sl[sw(l)];
+                const uint32_t x = xr | xl(k);
+                psi[base + x] = sp[sw2(l)];
+                if (BWD) lam[base + x] = sl[sw2(l)];
             }
         }
         __syncthreads();
     }
     if (BWD) {
-        const uint32_t nv = sg.nsec * 8;
+        const uint32_t nv = sg.nsec * 3;
         for (uint32_t i = tid; i < nv; i += kT) {
-            const uint32_t s = i >> 3, c = i & 7u;
+            const uint32_t s2 = i / 3, c = i % 3;
             double sum = 0.0;
-            for (int w = 0; w < kT / 32; ++w) sum += acc[(s * 8 + w) * 8 + c];
+            for (int w = 0; w < kWarps; ++w) sum += acc[(s2 * kWarps + w) * 3 + c];
             kpart[size_t(blockIdx.x) * nv + i] = sum;
         }
         __threadfence();
@@ -394,7 +377,7 @@ __global__ void __launch_bounds__(kT, 2) seg_c128(const C128Seg sg, const C128Op
             for (uint32_t i = tid; i < nv; i += kT) {
                 double sum = 0.0;
                 for (uint32_t b = 0; b < gridDim.x; ++b) sum += __ldcg(kpart + size_t(b) * nv + i);
-                K[size_t(sg.sec_begin) * 8 + i] = sum;
+                K[size_t(sg.sec_begin) * 3 + i] = sum;
             }
             if (tid == 0) *ticket = 0;
         }
@@ -403,7 +386,7 @@ __global__ void __launch_bounds__(kT, 2) seg_c128(const C128Seg sg, const C128Op
 
 } // namespace
 
-C128Plan build_c128_plan(const qf_gate *gates, size_t n_gates, uint32_t n) {
+C128Plan build_c128_plan(const qf_gate *gates, size_t n_gates, uint32_t n, uint64_t batch, int sms) {
     C128Plan P;
     for (size_t i = 0; i < n_gates; ++i) {
         const qf_gate &g = gates[i];
@@ -425,28 +408,35 @@ C128Plan build_c128_plan(const qf_gate *gates, size_t n_gates, uint32_t n) {
             P.ops.push_back({2u, g.q1, g.q0, 0u});
         }
     }
-    const uint32_t m = std::min<uint32_t>(n, kC128TileBits);
+    // op qubit (sections: the target; CNOT: the target) before the round fields reuse q
+    std::vector<uint32_t> opq(P.ops.size());
+    for (size_t i = 0; i < P.ops.size(); ++i) opq[i] = P.ops[i].q;
+    // tile bits: kC128TileBits, or 10 when the batch gives fewer tiles than SMs
+    // (measured at n = 12, batch 32: 0.84 ms at m = 10, 1.0 at m = 11, 1.55 at m = 8)
+    uint32_t m = std::min<uint32_t>(n, kC128TileBits);
+    if (m > 10 && (batch << (n - m)) < uint64_t(std::max(1, sms))) m = 10;
     const uint32_t nbase = std::min<uint32_t>(n, 3);
+    const uint32_t R = std::min<uint32_t>(m, 3);
     size_t i = 0;
     uint32_t sec = 0;
     while (i < P.ops.size() || (P.ops.empty() && P.segs.empty())) {
         std::set<uint32_t> S;
         for (uint32_t q = 0; q < nbase; ++q) S.insert(q);
-        uint32_t nsec = 0, ncz = 0, ncp = 0, cz0 = 0;
+        uint32_t nsec = 0, ncp = 0, cz0 = 0;
+        bool any_cz = false;
         size_t j = i;
         for (; j < P.ops.size(); ++j) {
             const C128Op &op = P.ops[j];
             const bool needs = op.type != 1;
-            if (needs && !S.count(op.q) && S.size() + 1 > m) break;
+            if (needs && !S.count(opq[j]) && S.size() + 1 > m) break;
             if (op.type == 0 && nsec == uint32_t(kC128MaxSec)) break;
-            if (op.type == 1 && ncz == uint32_t(kC128MaxCz)) break;
             if (j - i == size_t(kC128MaxOps)) break;
             if (op.type == 1 && ncp + op.b > uint32_t(kC128MaxCzPairs)) break;
-            if (needs) S.insert(op.q);
+            if (needs) S.insert(opq[j]);
             if (op.type == 0) ++nsec;
             if (op.type == 1) {
-                if (ncz == 0) cz0 = op.a;
-                P.ops[j].q = ncz++; // index of the CZ run within its segment
+                if (!any_cz) cz0 = op.a;
+                any_cz = true;
                 ncp += op.b;
             }
         }
@@ -470,6 +460,110 @@ C128Plan build_c128_plan(const qf_gate *gates, size_t n_gates, uint32_t n) {
                 sg.rq[r++] = uint8_t(q);
             }
         }
+        // ---- rounds: up to kC128RoundSecs sections on at most R local bits plus the
+        // CZ runs between them; a CNOT alone
+        sg.round_begin = uint32_t(P.rounds.size());
+        C128Round cur{};
+        bool open = false;
+        std::vector<uint32_t> cur_bits;
+        auto close = [&] {
+            if (!open) return;
+            // pad the register bits to R, preferring pads that leave a conflict-free
+            // quarter-warp (its three lowest thread bits distinct mod 3, sw2)
+            std::vector<uint32_t> best;
+            auto ok = [&](const std::vector<uint32_t> &bits) {
+                std::vector<uint32_t> thr;
+                for (uint32_t p = 0; p < m && thr.size() < 3; ++p)
+                    if (std::find(bits.begin(), bits.end(), p) == bits.end()) thr.push_back(p);
+                if (thr.size() < 3) return true;
+                return (thr[0] % 3) != (thr[1] % 3) && (thr[0] % 3) != (thr[2] % 3) && (thr[1] % 3) != (thr[2] % 3);
+            };
+            std::vector<uint32_t> bits = cur_bits;
+            std::function<bool(std::vector<uint32_t> &)> pad = [&](std::vector<uint32_t> &b) {
+                if (b.size() == R) return ok(b);
+                for (uint32_t p = 0; p < m; ++p) {
+                    if (std::find(b.begin(), b.end(), p) != b.end()) continue;
+                    b.push_back(p);
+                    if (pad(b)) return true;
+                    b.pop_back();
+                }
+                return false;
+            };
+            if (!pad(bits)) { // no conflict-free choice: lowest free positions
+                bits = cur_bits;
+                for (uint32_t p = 0; p < m && bits.size() < R; ++p)
+                    if (std::find(bits.begin(), bits.end(), p) == bits.end()) bits.push_back(p);
+            }
+            std::sort(bits.begin(), bits.end());
+            for (uint32_t k = 0; k < 4; ++k) {
+                cur.bits[k] = k < bits.size() ? uint8_t(bits[k]) : 0;
+                cur.gq[k] = k < bits.size() ? sg.lq[bits[k]] : 0;
+            }
+            for (uint32_t o = cur.op_begin; o < cur.op_end; ++o) {
+                C128Op &op = P.ops[o];
+                if (op.type == 0) {
+                    const uint32_t p = uint32_t(sg.lpos[opq[o]]);
+                    op.q = uint32_t(std::find(bits.begin(), bits.end(), p) - bits.begin());
+                } else if (op.type == 1) { // Q of every register offset j
+                    uint32_t qo = 0;
+                    for (uint32_t jo = 0; jo < (1u << R); ++jo) {
+                        uint32_t par = 0;
+                        for (uint32_t c = 0; c < op.b; ++c) {
+                            const uint32_t pr = P.cz[op.a + c], a = pr & 255u, b = pr >> 8;
+                            uint32_t ia = 4, ib = 4;
+                            for (uint32_t k = 0; k < bits.size(); ++k) {
+                                if (sg.lq[bits[k]] == a) ia = k;
+                                if (sg.lq[bits[k]] == b) ib = k;
+                            }
+                            if (ia < 4 && ib < 4) par ^= ((jo >> ia) & (jo >> ib)) & 1u;
+                        }
+                        qo |= par << jo;
+                    }
+                    op.q = qo;
+                }
+            }
+            P.rounds.push_back(cur);
+            open = false;
+        };
+        for (size_t o = i; o < j; ++o) {
+            const C128Op &op = P.ops[o];
+            if (op.type == 2) {
+                close();
+                C128Round rd{};
+                rd.kind = 1;
+                rd.op_begin = uint32_t(o);
+                rd.op_end = uint32_t(o + 1);
+                P.rounds.push_back(rd);
+                continue;
+            }
+            if (op.type == 0) {
+                const uint32_t p = uint32_t(sg.lpos[opq[o]]);
+                const bool have = std::find(cur_bits.begin(), cur_bits.end(), p) != cur_bits.end();
+                if (open && (cur.nsec == uint32_t(kC128RoundSecs) || (!have && cur_bits.size() == R))) close();
+                if (!open) {
+                    cur = C128Round{};
+                    cur.op_begin = uint32_t(o);
+                    cur_bits.clear();
+                    open = true;
+                }
+                if (std::find(cur_bits.begin(), cur_bits.end(), p) == cur_bits.end()) cur_bits.push_back(p);
+                P.ops[o].b = cur.nsec;                               // K slot
+                cur.sec[cur.nsec++] = uint8_t(P.ops[o].a - sec);     // section within the segment
+            } else {
+                if (!open) {
+                    cur = C128Round{};
+                    cur.op_begin = uint32_t(o);
+                    cur_bits.clear();
+                    open = true;
+                }
+                cur.has_cz = 1;
+            }
+            cur.op_end = uint32_t(o + 1);
+        }
+        close();
+        sg.round_end = uint32_t(P.rounds.size());
+        if (sg.round_end - sg.round_begin > uint32_t(kC128MaxRounds))
+            throw std::runtime_error("c128 plan: too many rounds in a segment");
         P.segs.push_back(sg);
         sec += nsec;
         if (j == i) break; // empty circuit: one segment that only copies
@@ -479,7 +573,7 @@ C128Plan build_c128_plan(const qf_gate *gates, size_t n_gates, uint32_t n) {
 }
 
 int c128_seg_grid(int sms, uint64_t tiles) {
-    const uint64_t cap = uint64_t(sms) * 2; // 2 CTAs/SM (backward: 80 KiB smem, <= 128 registers)
+    const uint64_t cap = uint64_t(sms) * 2; // 2 CTAs/SM (backward: 70 KiB smem, <= 128 registers)
     return int(std::max<uint64_t>(1, std::min(tiles, cap)));
 }
 
@@ -490,25 +584,44 @@ cudaError_t launch_c128_prep(cudaStream_t st, int nsec, const uint32_t *off, con
     return cudaGetLastError();
 }
 
+namespace {
+std::atomic<uint64_t> g_c128_attr{0};
+template <bool BWD, int R>
+void launch_seg(cudaStream_t st, int grid, size_t smem, const C128Seg &sg, const C128Op *ops,
+                const C128Round *rounds, const uint32_t *cz, const double2 *secU, double2 *psi,
+                double2 *lam, int n, uint64_t tiles, double *kpart, unsigned *ticket, double *K) {
+    seg_c128<BWD, R><<<grid, kT, smem, st>>>(sg, ops, rounds, cz, secU, psi, lam, n, tiles, kpart, ticket, K);
+}
+} // namespace
+
 cudaError_t launch_c128_segment(cudaStream_t st, bool backward, int grid, const C128Seg &sg,
-                                const C128Op *ops, const uint32_t *cz, const double2 *secU,
-                                double2 *psi, double2 *lam, int n, uint32_t batch, double *kpart,
-                                unsigned *ticket, double *K) {
+                                const C128Op *ops, const C128Round *rounds, const uint32_t *cz,
+                                const double2 *secU, double2 *psi, double2 *lam, int n, uint32_t batch,
+                                double *kpart, unsigned *ticket, double *K) {
     const uint64_t tiles = uint64_t(batch) << sg.nrest;
     const size_t amps = size_t(1) << sg.m;
+    const size_t smax = (size_t(2) << kC128TileBits) * sizeof(double2) + size_t(kC128MaxSec) * kWarps * 3 * sizeof(double);
+    const cudaError_t attr = once_per_device(g_c128_attr, [&] {
+        cudaError_t e = cudaSuccess;
+#define QF_C128_ATTR(B, R) \
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(seg_c128<B, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smax));
+        QF_C128_ATTR(true, 1) QF_C128_ATTR(true, 2) QF_C128_ATTR(true, 3)
+        QF_C128_ATTR(false, 1) QF_C128_ATTR(false, 2) QF_C128_ATTR(false, 3)
+#undef QF_C128_ATTR
+        return e;
+    });
+    if (attr != cudaSuccess) return attr;
+    const int R = int(std::min<uint32_t>(sg.m, 3u));
+    const size_t smem = amps * (backward ? 2 : 1) * sizeof(double2) +
+                        (backward ? size_t(std::max<uint32_t>(sg.nsec, 1)) * kWarps * 3 * sizeof(double) : 0);
     if (backward) {
-        const size_t smem = amps * 4 * sizeof(double2) + size_t(kC128MaxSec) * 64 * sizeof(double);
-        static std::atomic<uint64_t> done{0};
-        const cudaError_t attr = once_per_device(done, [] {
-            return cudaFuncSetAttribute(
-                seg_c128<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                int((size_t(4) << kC128TileBits) * sizeof(double2) + size_t(kC128MaxSec) * 64 * sizeof(double)));
-        });
-        if (attr != cudaSuccess) return attr;
-        seg_c128<true><<<grid, kT, smem, st>>>(sg, ops, cz, secU, psi, lam, n, tiles, kpart, ticket, K);
+        if (R == 3) launch_seg<true, 3>(st, grid, smem, sg, ops, rounds, cz, secU, psi, lam, n, tiles, kpart, ticket, K);
+        else if (R == 2) launch_seg<true, 2>(st, grid, smem, sg, ops, rounds, cz, secU, psi, lam, n, tiles, kpart, ticket, K);
+        else launch_seg<true, 1>(st, grid, smem, sg, ops, rounds, cz, secU, psi, lam, n, tiles, kpart, ticket, K);
     } else {
-        const size_t smem = amps * 2 * sizeof(double2);
-        seg_c128<false><<<grid, kT, smem, st>>>(sg, ops, cz, secU, psi, lam, n, tiles, kpart, ticket, K);
+        if (R == 3) launch_seg<false, 3>(st, grid, smem, sg, ops, rounds, cz, secU, psi, lam, n, tiles, kpart, ticket, K);
+        else if (R == 2) launch_seg<false, 2>(st, grid, smem, sg, ops, rounds, cz, secU, psi, lam, n, tiles, kpart, ticket, K);
+        else launch_seg<false, 1>(st, grid, smem, sg, ops, rounds, cz, secU, psi, lam, n, tiles, kpart, ticket, K);
     }
     return cudaGetLastError();
 }

@@ -890,7 +890,7 @@ void run_c128(qf_ctx *ctx, const qf_gate *gates, size_t n_gates, uint32_t n_qubi
     for (const qf_gate &g : P.gates)
         if (g.kind == QF_GATE_ROTATION) rp.push_back(g.param);
     const int n_rot = int(rp.size());
-    const C128Plan F = fused ? build_c128_plan(P.gates.data(), P.gates.size(), n) : C128Plan{};
+    const C128Plan F = fused ? build_c128_plan(P.gates.data(), P.gates.size(), n, batch, ctx->sms) : C128Plan{};
     const int nsec = int(F.sec_off.size());
     const int seg_grid = fused ? c128_seg_grid(ctx->sms, uint64_t(batch) << (n - F.segs[0].m)) : 0;
     const int gblocks = fused ? 0 : c128_gate_grid(std::max<uint64_t>(1, amps / 2));
@@ -933,6 +933,7 @@ void run_c128(qf_ctx *ctx, const qf_gate *gates, size_t n_gates, uint32_t n_qubi
     ck(cudaEventRecord(ev.a, s), "event"); // device time: kernels only (psi0 already resident)
     if (fused) {
         C128Op *ops = dupload(F.ops, owned);
+        C128Round *rounds = dupload(F.rounds, owned);
         uint32_t *cz = dupload(F.cz, owned);
         uint32_t *soff = dupload(F.sec_off, owned), *scnt = dupload(F.sec_cnt, owned),
                  *sgat = dupload(F.sec_gates, owned);
@@ -943,7 +944,7 @@ void run_c128(qf_ctx *ctx, const qf_gate *gates, size_t n_gates, uint32_t n_qubi
         ck(cudaMemsetAsync(ticket, 0, sizeof(unsigned), s), "memset");
         ck(launch_c128_prep(s, nsec, soff, scnt, sgat, th, secU), "c128 prep");
         for (const C128Seg &sg : F.segs) {
-            ck(launch_c128_segment(s, false, seg_grid, sg, ops, cz, secU, psi, lam, int(n), batch,
+            ck(launch_c128_segment(s, false, seg_grid, sg, ops, rounds, cz, secU, psi, lam, int(n), batch,
                                    kpart, ticket, K),
                "c128 segment");
             st.forward_passes++;
@@ -951,7 +952,7 @@ void run_c128(qf_ctx *ctx, const qf_gate *gates, size_t n_gates, uint32_t n_qubi
         ck(launch_seed_c128(s, int(n), batch, P.x_mask, P.z_mask, P.y_count, psi, lam, chunks, epart),
            "c128 seed");
         for (size_t i = F.segs.size(); i-- > 0;) {
-            ck(launch_c128_segment(s, true, seg_grid, F.segs[i], ops, cz, secU, psi, lam, int(n),
+            ck(launch_c128_segment(s, true, seg_grid, F.segs[i], ops, rounds, cz, secU, psi, lam, int(n),
                                    batch, kpart, ticket, K),
                "c128 segment");
             st.backward_passes++;

@@ -256,40 +256,58 @@ cudaError_t launch_reduce_c128(cudaStream_t st, const double *gpart, int gblocks
 // a *section* (maximal run of consecutive rotations on one qubit, one 2x2
 // unitary), a CZ run (one diagonal), a CNOT — cut into *segments*: op ranges
 // whose non-diagonal targets fit one shared-memory tile of 2^m amplitudes
-// (m = min(n, 10), local qubits 0..2 always included for coalescing). A segment
-// is one HBM pass; the backward measures K = sum psi_in lam_in^dag per section
-// and the gradients of the section's rotations are Re Tr(M_j K) (c128_finalize).
-constexpr int kC128TileBits = 10;
-constexpr int kC128MaxSec = 32; // sections per segment (shared K accumulators)
-constexpr int kC128MaxCz = 32;  // CZ runs per segment (one bit each in a register mask)
-constexpr int kC128MaxOps = 64;    // ops per segment (staged in shared memory)
+// (m = min(n, 11), local qubits 0..2 always included for coalescing). A segment
+// is one HBM pass. Inside it the ops are grouped into *rounds*: up to three
+// sections (on at most three local bits) and any CZ runs between them are applied
+// to eight register-resident amplitudes per thread between two shared-memory
+// transposes; a CNOT is a round of its own. The backward measures, per section,
+// X = Im(K01 + K10), Y = Re(K01 - K10), Z = Im(K00 - K11) of K = sum psi_in lam_in^dag
+// and the gradient of rotation j is (1/2)(hx X + hy Y + hz Z), H_j = sum_m h_m sigma_m
+// = B_j^dag g_j^dag P_j g_j B_j (c128_finalize).
+constexpr int kC128TileBits = 11;
+constexpr int kC128MaxSec = 32;      // sections per segment (shared K accumulators)
+constexpr int kC128MaxOps = 64;      // ops per segment (staged in shared memory)
+constexpr int kC128MaxRounds = 64;   // rounds per segment
 constexpr int kC128MaxCzPairs = 128; // CZ pairs per segment (staged in shared memory)
+constexpr int kC128RoundSecs = 3;    // sections per octet round (K accumulator slots)
 struct C128Op {
     uint32_t type; // 0 section, 1 CZ run, 2 CNOT
-    uint32_t q;    // section qubit / CNOT target / CZ run index within its segment
-    uint32_t a;    // section index / first CZ pair / CNOT control
-    uint32_t b;    // CZ pair count
+    uint32_t q;    // section: register bit in its round | CZ run: Q of the round's octet offsets
+                   // (bit j = parity of the run's pairs inside offset j) | CNOT: target qubit
+    uint32_t a;    // section: index (plan-wide) | CZ run: first pair (plan-wide) | CNOT: control qubit
+    uint32_t b;    // section: K slot in its round | CZ run: pair count
+};
+struct C128Round {
+    uint32_t kind;     // 0 octet round (sections / CZ runs), 1 CNOT
+    uint32_t op_begin, op_end;
+    uint32_t nsec;     // sections in the round (<= kC128RoundSecs)
+    uint32_t has_cz;   // the round applies a CZ run (needs the amplitudes' global indices)
+    uint8_t bits[4];   // octet: local positions of the register bits (ascending)
+    uint8_t gq[4];     // ... and their qubits
+    uint8_t sec[4];    // section (index within the segment) of K slot s
 };
 struct C128Seg {
-    uint32_t m, nrest, op_begin, op_end, sec_begin, nsec, cz_begin, cz_count;
+    uint32_t m, nrest, op_begin, op_end, sec_begin, nsec, cz_begin, cz_count, round_begin, round_end;
     int8_t lpos[32]; // qubit -> local bit, -1 if the qubit indexes tiles
     uint8_t lq[16];  // local bit -> qubit (ascending)
     uint8_t rq[32];  // tile bit -> qubit (ascending)
 };
 struct C128Plan {
     std::vector<C128Op> ops;
+    std::vector<C128Round> rounds;
     std::vector<C128Seg> segs;
     std::vector<uint32_t> cz;        // q0 | q1 << 8
     std::vector<uint32_t> sec_off, sec_cnt, sec_gates; // gates: axis | param << 2
 };
-C128Plan build_c128_plan(const qf_gate *gates, size_t n_gates, uint32_t n);
+C128Plan build_c128_plan(const qf_gate *gates, size_t n_gates, uint32_t n, uint64_t batch, int sms);
 int c128_seg_grid(int sms, uint64_t tiles);
 cudaError_t launch_c128_prep(cudaStream_t st, int nsec, const uint32_t *off, const uint32_t *cnt,
                              const uint32_t *gates, const double *theta, double2 *secU);
+// K: [section][3] (X, Y, Z); kpart: [grid][kC128MaxSec][3]
 cudaError_t launch_c128_segment(cudaStream_t st, bool backward, int grid, const C128Seg &sg,
-                                const C128Op *ops, const uint32_t *cz, const double2 *secU,
-                                double2 *psi, double2 *lam, int n, uint32_t batch, double *kpart,
-                                unsigned *ticket, double *K);
+                                const C128Op *ops, const C128Round *rounds, const uint32_t *cz,
+                                const double2 *secU, double2 *psi, double2 *lam, int n, uint32_t batch,
+                                double *kpart, unsigned *ticket, double *K);
 cudaError_t launch_c128_finalize(cudaStream_t st, int nsec, const uint32_t *off, const uint32_t *cnt,
                                  const uint32_t *gates, const double *theta, const double *K,
                                  double *grad);
