@@ -275,7 +275,7 @@ def measure(pkg, C, torch, dist, dev, rank, world, wl, batch_global, steps, warm
     gradients (+ the all-reduce) with CUDA events on the plan stream, max over
     ranks. Returns (line fields, plan, dp) -- the caller closes them."""
     import numpy as np
-    from paper_2603_02804_b200.parallel import DataParallelGradient, shard_range
+    from paper_2603_02804_b200.parallel import DataParallelGradient, HostInputPipeline, shard_range
     n, layers, k = wl["n"], wl["layers"], wl["ckpt"]
     a, b = shard_range(batch_global, rank, world)
     B = b - a
@@ -351,17 +351,27 @@ def measure(pkg, C, torch, dist, dev, rank, world, wl, batch_global, steps, warm
         stream.synchronize()
         barrier()
         torch.cuda.synchronize()
-        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        f0.record(stream)
-        for _ in range(steps):
-            dp.step_host(psi_h, theta_h, theta_d, res_h)
-        f1.record(stream)
+        # e2e: every step copies its own psi0 + theta from pinned host memory and reads
+        # [grad | loss] back; the psi0 copy of step i+1 overlaps step i (HostInputPipeline,
+        # double-buffered device inputs); timed from before the first copy to after the
+        # last D2H (host-synchronised wall clock, max over ranks)
+        pipe = HostInputPipeline(dp)
+        torch.cuda.synchronize()
+        barrier()
+        t0 = time.perf_counter()
+        pipe.run([psi_h] * steps, theta_h, theta_d, res_h)
         stream.synchronize()
-        e2e_ms = max_over_ranks(f0.elapsed_time(f1)) / steps
+        torch.cuda.synchronize()
+        e2e_ms = max_over_ranks((time.perf_counter() - t0) * 1000.0) / steps
+        pipe.copy_stream.synchronize()
+        dp.inputs = pipe  # the plan stays bound to the pipeline's buffers: keep them alive with dp
+        assert np.all(np.isfinite(res_h.numpy()))
         res["e2e"] = {"value": batch_global / (e2e_ms / 1000.0), "unit": "samples/s",
                       "h2d_bytes_per_step": int(psi_h.numel() * 4 + theta_h.numel() * 8),
                       "d2h_bytes_per_step": int(res_h.numel() * 8), "ms_per_step": e2e_ms,
-                      "api": "capi.Plan.upload_psi0 + qf_plan_gradient_device + all-reduce + D2H"}
+                      "api": "parallel.HostInputPipeline: pinned psi0/theta H2D per step (next "
+                             "step's copy overlapping this step), qf_plan_gradient_device, "
+                             "all-reduce, D2H of [grad | loss]"}
         if refsig and world == 1:
             # the reference-signature call: one-shot qf_gradient_c64 on PAGEABLE host
             # buffers (what qfuse::b200::run_checkpointed / gradient<float> do per

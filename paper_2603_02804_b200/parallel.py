@@ -37,6 +37,7 @@ class DataParallelGradient:
         m = plan.n_params
         self.out = torch_mod.empty(m + 1 + plan.batch, dtype=torch_mod.float64, device="cuda")
         self.m = m
+        self.inputs = None
 
     def step_device(self, theta_dev):
         torch = self.torch
@@ -52,6 +53,7 @@ class DataParallelGradient:
         if self.out is not None:
             self.stream.synchronize()
             self.out = None
+        self.inputs = None  # device input buffers a plan may still be bound to
 
     def step_host(self, psi0_pinned, theta_host_pinned, theta_dev, result_host):
         """End-to-end step with host buffers: H2D psi0 + theta, gradient,
@@ -63,6 +65,59 @@ class DataParallelGradient:
             self.step_device(theta_dev)
             result_host.copy_(self.out[: self.m + 1], non_blocking=True)
         return result_host
+
+
+class HostInputPipeline:
+    """End-to-end steps over a stream of host inputs with the next step's psi0
+    H2D overlapped with the current step's gradient (double-buffered device
+    copies, a copy stream; the plan reads them through qf_plan_set_psi0_device).
+    Every step still copies its own inputs from pinned host memory and reads its
+    [grad | loss] back; only the copy of step i+1 runs while step i computes."""
+
+    def __init__(self, dp):
+        torch = dp.torch
+        self.dp = dp
+        plan = dp.plan
+        vals = plan.batch * (2 << plan.n)
+        self.buf = [torch.empty(vals, dtype=torch.float32, device="cuda") for _ in range(2)]
+        self.copy_stream = torch.cuda.Stream()
+        self.copied = [torch.cuda.Event(), torch.cuda.Event()]
+        self.done = [torch.cuda.Event(), torch.cuda.Event()]
+        self.used = [False, False]
+
+    def _issue_copy(self, slot, psi0_pinned):
+        torch = self.dp.torch
+        with torch.cuda.stream(self.copy_stream):
+            if self.used[slot]:  # the step that last read this buffer has finished
+                self.copy_stream.wait_event(self.done[slot])
+            self.buf[slot].copy_(psi0_pinned, non_blocking=True)
+            self.copied[slot].record(self.copy_stream)
+
+    def run(self, psi0_list, theta_host_pinned, theta_dev, result_host):
+        """Steps i = 0..len-1 on psi0_list[i] (pinned float32, batch * 2^(n+1)
+        values each); result_host (pinned float64, M + 1) holds the last step's
+        [grad | loss] once the plan stream is synchronized."""
+        dp, torch = self.dp, self.dp.torch
+        if not psi0_list:
+            return result_host
+        self._issue_copy(0, psi0_list[0])
+        for i in range(len(psi0_list)):
+            slot = i % 2
+            if i + 1 < len(psi0_list):
+                self._issue_copy(1 - slot, psi0_list[i + 1])
+            with torch.cuda.stream(dp.stream):
+                dp.stream.wait_event(self.copied[slot])
+                dp.plan.set_psi0_device(self.buf[slot].data_ptr())
+                theta_dev.copy_(theta_host_pinned, non_blocking=True)
+                dp.step_device(theta_dev)
+                result_host.copy_(dp.out[: dp.m + 1], non_blocking=True)
+                self.done[slot].record(dp.stream)
+                self.used[slot] = True
+        return result_host
+
+    def close(self):
+        self.copy_stream.synchronize()
+        self.buf = []
 
 
 def combine_partials(partials):

@@ -153,3 +153,30 @@ def test_bench_two_ranks_gloo():
         assert line["n_gpus"] == 2 and line["scaling"] == scaling
         assert line["config"]["global_batch"] == glob and line["config"]["batch_per_gpu"] == 8
         assert line["value"] > 0 and line["e2e"]["value"] > 0
+
+
+def test_host_input_pipeline_matches_direct(ctx):
+    """parallel.HostInputPipeline (the bench's e2e leg): three steps on three
+    different host psi0 with the next copy overlapping the current step; the
+    result of the last step equals the direct plan gradient on that psi0, and
+    the plan still accepts its own uploads afterwards."""
+    from paper_2603_02804_b200.parallel import DataParallelGradient, HostInputPipeline
+    n, layers, batch = 14, 3, 3
+    gates, npar, theta, _, pauli = _case(n, layers, batch)
+    plan = capi.Plan(ctx, gates, n, npar, layers, 0, batch, pauli)
+    dp = DataParallelGradient(plan, torch)
+    psis = [torch.from_numpy(C.new_random_state(n, batch, 50 + i).reshape(-1).copy()).pin_memory()
+            for i in range(3)]
+    th_h = torch.from_numpy(theta.copy()).pin_memory()
+    th_d = th_h.to("cuda")
+    res_h = torch.empty(npar + 1, dtype=torch.float64).pin_memory()
+    pipe = HostInputPipeline(dp)
+    pipe.run(psis, th_h, th_d, res_h)
+    dp.stream.synchronize()
+    got = res_h.numpy().copy()
+    plan.upload_psi0(psis[-1].numpy().reshape(batch, 1 << n, 2))
+    ref = plan.gradient(theta)
+    assert rel_diff(got[:npar], ref.gradient) <= 1e-12
+    assert got[npar] == pytest.approx(ref.loss, rel=1e-12, abs=1e-15)
+    dp.close()
+    plan.close()
