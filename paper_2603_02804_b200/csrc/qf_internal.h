@@ -110,6 +110,10 @@ constexpr uint32_t kProgB16x = prog_encode(3, kProgB16xPh, 0xF0Fu);
 // row qubits and round 1 on rows + columns (4 phases, 20 Ry each).
 constexpr PassPhase kProgAltPh[4] = {{1, 1}, {2, 7}, {1, 4}, {0, 4}};
 constexpr uint32_t kProgAlt = prog_encode(4, kProgAltPh, 0xFFFu);
+// 17 <= n <= 19: layout B rotates only some of group 1's row bits (runtime bit
+// checks in that group; the encoding keeps the FULL flags, not the bit pattern)
+constexpr uint32_t kProgB20P = prog_encode(3, kProgB20Ph, 0xF20u);
+constexpr uint32_t kProgAltP = prog_encode(4, kProgAltPh, 0xF2Fu);
 
 struct PassParams {
     int n;

@@ -224,7 +224,10 @@ __global__ void __launch_bounds__(kDualThreads, 1)
     const uint32_t gtid = tid & 255u;
     // light passes (layout B) are bound by the one-tile-deep ring: their next ring
     // load is prefetched into L2 (QF_L2PF=0 disables)
-    const bool L2PF = PROG != 0 && prog_nph(PROG) <= 3 && p.l2pf;
+#ifndef QF_L2PF_NPH
+#define QF_L2PF_NPH 3
+#endif
+    const bool L2PF = PROG != 0 && prog_nph(PROG) <= QF_L2PF_NPH && p.l2pf;
 
     const int lo_mask = (1 << p.tile_lo_bits) - 1, hi_mask = (1 << p.tile_hi_bits) - 1;
     const int sample_shift = p.tile_lo_bits + p.tile_hi_bits;
@@ -393,6 +396,9 @@ cudaError_t ensure_attrs() {
         if (e == cudaSuccess) e = set_smem(pass_bwd_dual<kProgB16>, dual_smem());
         if (e == cudaSuccess) e = set_smem(pass_bwd_dual<kProgB16x>, dual_smem());
         if (e == cudaSuccess) e = set_smem(pass_bwd_dual<kProgAlt>, dual_smem());
+        if (e == cudaSuccess) e = set_smem(pass_kernel<false, 2, kProgB20P>, pass_smem(false, 2));
+        if (e == cudaSuccess) e = set_smem(pass_bwd_dual<kProgB20P>, dual_smem());
+        if (e == cudaSuccess) e = set_smem(pass_bwd_dual<kProgAltP>, dual_smem());
         return e;
     });
 }
@@ -444,15 +450,14 @@ cudaError_t launch_pass(cudaStream_t st, bool backward, int grid, const PassPara
     const CUtensorMap &l = lam ? *lam : *psi_out;
     // straight-line kernels for the compiled programs (Z is measured at stage 0 only:
     // those passes take the runtime-dispatch kernel)
-    uint32_t prog = progs_enabled() && !(backward && p.zmask) ? p.prog : 0u;
-    static const bool ablate_alt = getenv("QF_ABLATE_ALT") && atoi(getenv("QF_ABLATE_ALT"));
-    if (ablate_alt && backward && (prog == kProgA || prog == kProgB20)) prog = kProgAlt; // timing only
+    const uint32_t prog = progs_enabled() && !(backward && p.zmask) ? p.prog : 0u;
     if (!backward) {
         const size_t sm = pass_smem(false, 2);
         if (prog == kProgA) pass_kernel<false, 2, kProgA><<<grid, kThreads, sm, st>>>(p, *psi_in, *psi_out, l);
         else if (prog == kProgB20) pass_kernel<false, 2, kProgB20><<<grid, kThreads, sm, st>>>(p, *psi_in, *psi_out, l);
         else if (prog == kProgB16) pass_kernel<false, 2, kProgB16><<<grid, kThreads, sm, st>>>(p, *psi_in, *psi_out, l);
         else if (prog == kProgB16x) pass_kernel<false, 2, kProgB16x><<<grid, kThreads, sm, st>>>(p, *psi_in, *psi_out, l);
+        else if (prog == kProgB20P) pass_kernel<false, 2, kProgB20P><<<grid, kThreads, sm, st>>>(p, *psi_in, *psi_out, l);
         else pass_kernel<false, 2><<<grid, kThreads, sm, st>>>(p, *psi_in, *psi_out, l);
     } else if (bwd_pipe() == 3) {
         pass_kernel<true, 3><<<grid, kThreads, pass_smem(true, 3), st>>>(p, *psi_in, *psi_out, l);
@@ -463,6 +468,8 @@ cudaError_t launch_pass(cudaStream_t st, bool backward, int grid, const PassPara
         else if (prog == kProgB16) pass_bwd_dual<kProgB16><<<grid, kDualThreads, sm, st>>>(p, *psi_in, *psi_out, l);
         else if (prog == kProgB16x) pass_bwd_dual<kProgB16x><<<grid, kDualThreads, sm, st>>>(p, *psi_in, *psi_out, l);
         else if (prog == kProgAlt) pass_bwd_dual<kProgAlt><<<grid, kDualThreads, sm, st>>>(p, *psi_in, *psi_out, l);
+        else if (prog == kProgB20P) pass_bwd_dual<kProgB20P><<<grid, kDualThreads, sm, st>>>(p, *psi_in, *psi_out, l);
+        else if (prog == kProgAltP) pass_bwd_dual<kProgAltP><<<grid, kDualThreads, sm, st>>>(p, *psi_in, *psi_out, l);
         else pass_bwd_dual<0><<<grid, kDualThreads, sm, st>>>(p, *psi_in, *psi_out, l);
     } else {
         pass_kernel<true, 1><<<grid, kThreads, pass_smem(true, 1), st>>>(p, *psi_in, *psi_out, l);

@@ -396,11 +396,14 @@ Plan make_plan(const qf_gate *gates, size_t n_gates, uint32_t n, uint32_t n_para
         const uint32_t pps = static_cast<uint32_t>(std::max(1, NL - 1));
         plan.ckpt_passes = k * pps;
         const size_t np = plan.steps.size();
-        // balanced backward (Plan::alt): n = 20 with layouts A (12 rotated) and B (rows
-        // 12..19), strict A/B alternation with pass p applying D_p, an even slot period
+        // balanced backward (Plan::alt): 17 <= n <= 20 with layouts A (12 rotated) and B
+        // (top rows 12..n-1), strict A/B alternation with pass p applying D_p, an even
+        // slot period
         const char *ea = getenv("QF_ALT");
-        bool alt = (!ea || atoi(ea) != 0) && n == 20 && NL == 2 && plan.layouts[0].rot_mask == 0xFFFu &&
-                   plan.layouts[0].gd == 0 && plan.layouts[1].rot_mask == 0xFF0u && plan.layouts[1].gd == 2 &&
+        const uint32_t rowsB = plan.layouts.size() >= 2 ? plan.layouts[1].rot_mask : 0u;
+        bool alt = (!ea || atoi(ea) != 0) && n >= 17 && n <= 20 && NL == 2 &&
+                   plan.layouts[0].rot_mask == 0xFFFu && plan.layouts[0].gd == 0 &&
+                   (rowsB & 0xF0Fu) == 0xF00u && (rowsB & 0x0F0u) != 0u && plan.layouts[1].gd == 2 &&
                    plan.ckpt_passes % 2 == 0 && np >= 2;
         for (size_t pi = 0; alt && pi < np; ++pi) {
             const PassStep &ps = plan.steps[pi];
@@ -427,8 +430,9 @@ Plan make_plan(const qf_gate *gates, size_t n_gates, uint32_t n, uint32_t n_para
             for (const PassStep &ps : plan.steps) {
                 // round 0: the layout's 8 row qubits; D; round 1: rows + columns
                 PassStep b = ps;
-                b.rot0 = ps.s0 >= 0 ? 0xFF0u : 0u;
-                b.rot1 = ps.s1 >= 0 ? 0xFFFu : 0u;
+                const uint32_t rows = ps.layout == 0 ? 0xFF0u : rowsB;
+                b.rot0 = ps.s0 >= 0 ? rows : 0u;
+                b.rot1 = ps.s1 >= 0 ? (rows | 0x00Fu) : 0u;
                 b.nph = 0;
                 auto add = [&](int g, uint8_t ops) { b.ph[b.nph++] = PassPhase{int8_t(g), ops}; };
                 const uint8_t gd_ops = uint8_t((ps.s0 >= 0 ? 1 : 0) | (ps.sd >= 0 ? 2 : 0) | (ps.s1 >= 0 ? 4 : 0));

@@ -694,12 +694,14 @@ def test_config2_depth_vs_oracle(ctx, oracle):
     _check(res, oracle.gradient(gates, n, npar, psi0, theta, pauli))
 
 
-@pytest.mark.parametrize("n", [17, 18, 19])
-def test_hea_17_19_deep_vs_oracle(ctx, oracle, n):
+@pytest.mark.parametrize("n,k", [(17, 10), (18, 10), (19, 10), (17, 5), (19, 5)])
+def test_hea_17_19_deep_vs_oracle(ctx, oracle, n, k):
     """HEA n = 17..19 (streaming, layouts A/B with 5..7 top qubits rotated in
-    B) at 20 layers, k = 10, against the fp64 oracle."""
+    B) at 20 layers against the fp64 oracle: k = 10 runs the balanced backward
+    (kProgAlt / kProgAltP), k = 5 (odd slot period) the plain one (kProgA /
+    kProgB20P)."""
     gates, npar, theta, psi0, pauli = _hea_case(n, 20, 1, seed=300 + n)
-    res = capi.gradient_c64(ctx, gates, n, npar, 20, 10, psi0, theta, pauli)
+    res = capi.gradient_c64(ctx, gates, n, npar, 20, k, psi0, theta, pauli)
     _check(res, oracle.gradient(gates, n, npar, psi0, theta, pauli))
 
 
