@@ -114,6 +114,8 @@ constexpr uint32_t kProgAlt = prog_encode(4, kProgAltPh, 0xFFFu);
 // checks in that group; the encoding keeps the FULL flags, not the bit pattern)
 constexpr uint32_t kProgB20P = prog_encode(3, kProgB20Ph, 0xF20u);
 constexpr uint32_t kProgAltP = prog_encode(4, kProgAltPh, 0xF2Fu);
+// 13 <= n <= 15: layout B rotates the columns and only part of group 2 (qubits 12..n-1)
+constexpr uint32_t kProgB16xP = prog_encode(3, kProgB16xPh, 0x20Fu);
 
 struct PassParams {
     int n;

@@ -399,6 +399,8 @@ cudaError_t ensure_attrs() {
         if (e == cudaSuccess) e = set_smem(pass_kernel<false, 2, kProgB20P>, pass_smem(false, 2));
         if (e == cudaSuccess) e = set_smem(pass_bwd_dual<kProgB20P>, dual_smem());
         if (e == cudaSuccess) e = set_smem(pass_bwd_dual<kProgAltP>, dual_smem());
+        if (e == cudaSuccess) e = set_smem(pass_kernel<false, 2, kProgB16xP>, pass_smem(false, 2));
+        if (e == cudaSuccess) e = set_smem(pass_bwd_dual<kProgB16xP>, dual_smem());
         return e;
     });
 }
@@ -458,6 +460,7 @@ cudaError_t launch_pass(cudaStream_t st, bool backward, int grid, const PassPara
         else if (prog == kProgB16) pass_kernel<false, 2, kProgB16><<<grid, kThreads, sm, st>>>(p, *psi_in, *psi_out, l);
         else if (prog == kProgB16x) pass_kernel<false, 2, kProgB16x><<<grid, kThreads, sm, st>>>(p, *psi_in, *psi_out, l);
         else if (prog == kProgB20P) pass_kernel<false, 2, kProgB20P><<<grid, kThreads, sm, st>>>(p, *psi_in, *psi_out, l);
+        else if (prog == kProgB16xP) pass_kernel<false, 2, kProgB16xP><<<grid, kThreads, sm, st>>>(p, *psi_in, *psi_out, l);
         else pass_kernel<false, 2><<<grid, kThreads, sm, st>>>(p, *psi_in, *psi_out, l);
     } else if (bwd_pipe() == 3) {
         pass_kernel<true, 3><<<grid, kThreads, pass_smem(true, 3), st>>>(p, *psi_in, *psi_out, l);
@@ -470,6 +473,7 @@ cudaError_t launch_pass(cudaStream_t st, bool backward, int grid, const PassPara
         else if (prog == kProgAlt) pass_bwd_dual<kProgAlt><<<grid, kDualThreads, sm, st>>>(p, *psi_in, *psi_out, l);
         else if (prog == kProgB20P) pass_bwd_dual<kProgB20P><<<grid, kDualThreads, sm, st>>>(p, *psi_in, *psi_out, l);
         else if (prog == kProgAltP) pass_bwd_dual<kProgAltP><<<grid, kDualThreads, sm, st>>>(p, *psi_in, *psi_out, l);
+        else if (prog == kProgB16xP) pass_bwd_dual<kProgB16xP><<<grid, kDualThreads, sm, st>>>(p, *psi_in, *psi_out, l);
         else pass_bwd_dual<0><<<grid, kDualThreads, sm, st>>>(p, *psi_in, *psi_out, l);
     } else {
         pass_kernel<true, 1><<<grid, kThreads, pass_smem(true, 1), st>>>(p, *psi_in, *psi_out, l);

@@ -58,7 +58,7 @@ def test_config1_observables(ctx, oracle, label, loss_ref, gsum_ref):
 @pytest.mark.parametrize("n,layers,batch", [
     (2, 3, 5), (3, 2, 3), (4, 1, 1), (5, 4, 7), (6, 8, 4), (8, 5, 3), (10, 4, 2),
     (11, 3, 3), (12, 6, 2),          # sample-resident kernel
-    (13, 2, 2), (14, 3, 2), (16, 2, 1),  # streaming passes A + B
+    (13, 2, 2), (14, 3, 2), (15, 4, 1), (16, 2, 1),  # streaming passes A + B
 ])
 def test_hea_sizes(ctx, oracle, n, layers, batch):
     gates, npar, theta, psi0, pauli = _hea_case(n, layers, batch, seed=77 + n)
