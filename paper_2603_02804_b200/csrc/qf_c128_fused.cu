@@ -66,6 +66,12 @@ __device__ __forceinline__ Cx2 rot(int axis, double c, double s) {
     return {make_double2(c, -s), z, z, make_double2(c, s)};
 }
 
+// Per section: U (the rotations multiplied in fp64, later gates on the left, like
+// compose_block_unitary fusion.cpp:127-152), then U = e^{i d} Rz(a) Ry(b) Rz(g) in
+// fp64 and the round data of it (kC128SecWords double2):
+//   [0] (p, q): Ry(b) = m [[p, -q], [q, p]] with (p, q) = (1, tan b/2), m = cos b/2
+//       when cos >= sin, else (cot b/2, 1), m = sin b/2 (two DFMA per output either way)
+//   [1] (m, g)   [2], [3] e^{-ig/2}, e^{+ig/2}   [4], [5] e^{id} e^{-ia/2}, e^{id} e^{+ia/2}
 __global__ void c128_prep(int nsec, const uint32_t *off, const uint32_t *cnt, const uint32_t *gates,
                           const double *theta, double2 *secU) {
     const int s = blockIdx.x * blockDim.x + threadIdx.x;
@@ -77,20 +83,48 @@ __global__ void c128_prep(int nsec, const uint32_t *off, const uint32_t *cnt, co
         sincos(theta[g >> 2] / 2.0, &sn, &cs);
         U = mul(rot(int(g & 3u), cs, sn), U);
     }
-    secU[4 * s + 0] = U.a;
-    secU[4 * s + 1] = U.b;
-    secU[4 * s + 2] = U.c;
-    secU[4 * s + 3] = U.d;
+    const double2 det = cadd(cm(U.a, U.d), make_double2(-(U.b.x * U.c.x - U.b.y * U.c.y),
+                                                        -(U.b.x * U.c.y + U.b.y * U.c.x)));
+    const double d = 0.5 * atan2(det.y, det.x);
+    double sd, cd;
+    sincos(-d, &sd, &cd);
+    const double2 ph = make_double2(cd, sd);             // e^{-id}
+    const double2 a = cm(ph, U.a), b = cm(ph, U.c);      // V = e^{-id} U in SU(2): V00, V10
+    const double c = hypot(a.x, a.y), sn = hypot(b.x, b.y);
+    const double arga = c > 0.0 ? atan2(a.y, a.x) : 0.0, argb = sn > 0.0 ? atan2(b.y, b.x) : 0.0;
+    const double al = argb - arga, ga = -arga - argb;    // a + g = -2 arg V00, a - g = 2 arg V10
+    double2 *w = secU + size_t(s) * kC128SecWords;
+    if (c >= sn) {
+        w[0] = make_double2(1.0, sn / c);
+        w[1] = make_double2(c, ga);
+    } else {
+        w[0] = make_double2(c / sn, 1.0);
+        w[1] = make_double2(sn, ga);
+    }
+    double sg, cg, sa, ca;
+    sincos(0.5 * ga, &sg, &cg);
+    sincos(0.5 * al, &sa, &ca);
+    w[2] = make_double2(cg, -sg);
+    w[3] = make_double2(cg, sg);
+    const double2 ed = make_double2(cd, -sd);            // e^{+id}
+    w[4] = cm(ed, make_double2(ca, -sa));
+    w[5] = cm(ed, make_double2(ca, sa));
 }
 
 // K per section: (X, Y, Z); grad of rotation j = (1/2)(hx X + hy Y + hz Z) with
 // H_j = B_j^dag g_j^dag P_j g_j B_j = [[hz, hx - i hy], [hx + i hy, -hz]].
 __global__ void c128_finalize(int nsec, const uint32_t *off, const uint32_t *cnt,
-                              const uint32_t *gates, const double *theta, const double *K,
-                              double *grad) {
+                              const uint32_t *gates, const double *theta, const double2 *secU,
+                              const double *K, double *grad) {
     const int s = blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= nsec) return;
     const double X = K[size_t(s) * 3 + 0], Y = K[size_t(s) * 3 + 1], Z = K[size_t(s) * 3 + 2];
+    // K was measured after the section's Rz(g) (the rounds apply all Rz(g) of a round
+    // first): K' = G K G^dag, G = Rz(g), so Re Tr(M K) = Re Tr(G M G^dag K')
+    const double gam = secU[size_t(s) * kC128SecWords + 1].y;
+    double sg, cg;
+    sincos(0.5 * gam, &sg, &cg);
+    const Cx2 G = {make_double2(cg, -sg), make_double2(0, 0), make_double2(0, 0), make_double2(cg, sg)};
     Cx2 B = ident();
     for (uint32_t i = 0; i < cnt[s]; ++i) {
         const uint32_t g = gates[off[s] + i];
@@ -99,7 +133,7 @@ __global__ void c128_finalize(int nsec, const uint32_t *off, const uint32_t *cnt
         sincos(theta[g >> 2] / 2.0, &sn, &cs);
         const Cx2 u = rot(axis, cs, sn), P = rot(axis, 0.0, 1.0); // rot(axis, 0, 1) = -i P
         const Cx2 uB = mul(u, B);
-        const Cx2 H = mul(dag(uB), mul(P, uB)); // = -i B^dag g^dag P g B
+        const Cx2 H = mul(G, mul(mul(dag(uB), mul(P, uB)), dag(G))); // = -i G B^dag g^dag P g B G^dag
         // H holds -i H_j: hz = Re H_j00 = -Im H00, hx + i hy = H_j10 = i H10
         const double hz = -H.a.y, hx = -H.c.y, hy = H.c.x;
         grad[g >> 2] = 0.5 * (hx * X + hy * Y + hz * Z);
@@ -126,29 +160,26 @@ __device__ __forceinline__ void cp_async16(void *smem_dst, const void *gmem_src)
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
-struct U2 { // a section's unitary, or its adjoint
-    double2 u00, u01, u10, u11;
-};
-__device__ __forceinline__ U2 load_u(const double2 *u, bool adjoint) {
-    const double2 a = u[0], b = u[1], c = u[2], d = u[3];
-    return adjoint ? U2{cj(a), cj(c), cj(b), cj(d)} : U2{a, b, c, d};
-}
-// a' = u00 a + u01 b, b' = u10 a + u11 b: four independent FMA chains (one DMUL +
-// three DFMA per component, 16 FP64 instructions per pair)
-__device__ __forceinline__ double2 cmac2(double2 x, double2 a, double2 y, double2 b) {
-    return make_double2(fma(x.x, a.x, fma(-x.y, a.y, fma(y.x, b.x, -y.y * b.y))),
-                        fma(x.x, a.y, fma(x.y, a.x, fma(y.x, b.y, y.y * b.x))));
-}
-__device__ __forceinline__ void apply_u(const U2 &u, double2 &a, double2 &b) {
-    const double2 a0 = a, b0 = b;
-    a = cmac2(u.u00, a0, u.u01, b0);
-    b = cmac2(u.u10, a0, u.u11, b0);
-}
-// section on register bit B of the 2^R amplitudes
-template <int B, int R> __device__ __forceinline__ void apply_bit(const U2 &u, double2 (&v)[1 << R]) {
+// Unscaled Ry on register bit B: forward R'(p, q) = [[p, -q], [q, p]], inverse R'(p, -q);
+// (p, q) = (1, t) (fa) or (t', 1): one DFMA per output component.
+template <int B, int R, bool INV>
+__device__ __forceinline__ void ry_bit(bool fa, double2 pq, double2 (&v)[1 << R]) {
+    const double t = fa ? pq.y : pq.x;
 #pragma unroll
-    for (int j = 0; j < (1 << R); ++j)
-        if (!(j & (1 << B))) apply_u(u, v[j], v[j | (1 << B)]);
+    for (int j = 0; j < (1 << R); ++j) {
+        if (j & (1 << B)) continue;
+        const double2 a = v[j], b = v[j | (1 << B)];
+        if (fa) { // a' = a -+ t b, b' = b +- t a
+            const double tt = INV ? t : -t;
+            v[j] = make_double2(fma(tt, b.x, a.x), fma(tt, b.y, a.y));
+            v[j | (1 << B)] = make_double2(fma(-tt, a.x, b.x), fma(-tt, a.y, b.y));
+        } else { // forward a' = t a - b, b' = a + t b; inverse a' = t a + b, b' = t b - a
+            v[j] = INV ? make_double2(fma(t, a.x, b.x), fma(t, a.y, b.y))
+                       : make_double2(fma(t, a.x, -b.x), fma(t, a.y, -b.y));
+            v[j | (1 << B)] = INV ? make_double2(fma(t, b.x, -a.x), fma(t, b.y, -a.y))
+                                  : make_double2(fma(t, b.x, a.x), fma(t, b.y, a.y));
+        }
+    }
 }
 // (X, Y, Z) of register bit B: X += Im(a lb* + b la*), Y += Re(a lb* - b la*),
 // Z += Im(a la* - b lb*)   (a, b = psi of the pair, la, lb = lambda)
@@ -184,13 +215,17 @@ __global__ void __launch_bounds__(kT, 2) seg_c128(const C128Seg sg, const C128Op
     extern __shared__ double2 sm[];
     const uint32_t m = sg.m, amps = 1u << m;
     double2 *sp = sm, *sl = sm + amps;
-    double *acc = reinterpret_cast<double *>(sm + (BWD ? 2u : 1u) * amps); // [sec][warp][3]
+    // round tables: [round][16] = Dg[8] (all Rz(g) of the round), Da'[8] (all Rz(a),
+    // the global phases and the Ry scales m), then [round][4] K scales; then K slots
+    double2 *rtab = sm + (BWD ? 2u : 1u) * amps;
+    double *kscl = reinterpret_cast<double *>(rtab + size_t(kC128MaxRounds) * 16);
+    double *acc = kscl + size_t(kC128MaxRounds) * 4; // [sec][warp][3]
     const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31u;
     __shared__ int8_t lpos[32];
     __shared__ uint8_t lq[16], rq[32];
     __shared__ C128Op ops_s[kC128MaxOps];
     __shared__ C128Round rnd_s[kC128MaxRounds];
-    __shared__ double2 u_s[kC128MaxSec * 4];
+    __shared__ double2 u_s[kC128MaxSec * kC128SecWords];
     __shared__ uint32_t cz_s[kC128MaxCzPairs];
     if (tid == 0) { // constant indices: no local copy of the parameter block
 #pragma unroll
@@ -203,10 +238,33 @@ __global__ void __launch_bounds__(kT, 2) seg_c128(const C128Seg sg, const C128Op
     const uint32_t nops = sg.op_end - sg.op_begin, nrnd = sg.round_end - sg.round_begin;
     for (uint32_t i = tid; i < nops; i += kT) ops_s[i] = ops[sg.op_begin + i];
     for (uint32_t i = tid; i < nrnd; i += kT) rnd_s[i] = rounds[sg.round_begin + i];
-    for (uint32_t i = tid; i < sg.nsec * 4; i += kT) u_s[i] = secU[size_t(sg.sec_begin) * 4 + i];
+    for (uint32_t i = tid; i < sg.nsec * kC128SecWords; i += kT)
+        u_s[i] = secU[size_t(sg.sec_begin) * kC128SecWords + i];
     for (uint32_t i = tid; i < sg.cz_count; i += kT) cz_s[i] = czp[sg.cz_begin + i];
     if (BWD)
         for (uint32_t i = tid; i < sg.nsec * kWarps * 3; i += kT) acc[i] = 0.0;
+    __syncthreads();
+    for (uint32_t w = tid; w < nrnd * 16; w += kT) { // Dg / Da' entries of every round
+        const C128Round rd = rnd_s[w >> 4];
+        if (rd.kind != 0) continue;
+        const uint32_t j = w & 7u, alpha = (w >> 3) & 1u;
+        double2 f = make_double2(1.0, 0.0);
+        for (uint32_t k = 0; k < rd.nsec; ++k) {
+            const double2 *u = u_s + rd.sec[k] * kC128SecWords;
+            const uint32_t bit = (j >> rd.sbit[k]) & 1u;
+            f = cm(f, u[(alpha ? 4 : 2) + bit]);
+            if (alpha) f = make_double2(f.x * u[1].x, f.y * u[1].x);
+        }
+        rtab[w] = f;
+        if (j == 0 && !alpha) { // K slot k is measured with psi, lambda off by f = prod_{l<k} m_l
+            double sc = 1.0;    // (the scales of the slots not undone yet): K carries f^2
+            for (uint32_t k = 0; k < rd.nsec; ++k) {
+                kscl[(w >> 4) * 4 + k] = sc;
+                const double m = u_s[rd.sec[k] * kC128SecWords + 1].x;
+                sc /= m * m;
+            }
+        }
+    }
     __syncthreads();
     constexpr int KA = (1 << kC128TileBits) / kT; // tile amplitudes per thread (copy in / out)
     // local part of their global index (recomputed at the copies: fewer live registers
@@ -243,7 +301,8 @@ __global__ void __launch_bounds__(kT, 2) seg_c128(const C128Seg sg, const C128Op
         cp_async_wait_all();
         __syncthreads();
         for (uint32_t ri = 0; ri < nrnd; ++ri) {
-            const C128Round rd = rnd_s[BWD ? nrnd - 1 - ri : ri];
+            const uint32_t rix = BWD ? nrnd - 1 - ri : ri;
+            const C128Round rd = rnd_s[rix];
             if (rd.kind == 1) { // CNOT(control a, target q): pair swaps, self-inverse
                 const C128Op op = ops_s[rd.op_begin - sg.op_begin];
                 const uint32_t pos = uint32_t(lpos[op.q]);
@@ -290,20 +349,37 @@ __global__ void __launch_bounds__(kT, 2) seg_c128(const C128Seg sg, const C128Op
                         x0 = xr;
                         for (uint32_t j = 0; j < m; ++j) x0 |= ((bl >> j) & 1u) << lq[j];
                     }
+                    // e^{id} Rz(a) Ry(b) Rz(g) per section: all Rz(g) of the round first (Dg),
+                    // the unscaled Ry (two DFMA per output), all Rz(a), phases and Ry scales last
+                    // (Da'); CZ runs in place. The backward runs the inverse: conj(Da') (the
+                    // scales m stay in it: R'^-1 = m^2 R'(p, -q)), R'(p, -q), conj(Dg).
+                    const double2 *tb = rtab + size_t(rix) * 16;
+                    if (BWD) {
+#pragma unroll
+                        for (int j = 0; j < NV; ++j) {
+                            const double2 f = cj(tb[8 + j]);
+                            v[j] = cm(f, v[j]);
+                            w[j] = cm(f, w[j]);
+                        }
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < NV; ++j) v[j] = cm(tb[j], v[j]);
+                    }
                     const uint32_t no = rd.op_end - rd.op_begin;
                     for (uint32_t oi = 0; oi < no; ++oi) {
                         const C128Op op = ops_s[(BWD ? rd.op_end - 1 - oi : rd.op_begin + oi) - sg.op_begin];
                         if (op.type == 0) {
-                            const U2 u = load_u(u_s + (op.a - sg.sec_begin) * 4, BWD);
+                            const double2 pq = u_s[(op.a - sg.sec_begin) * kC128SecWords];
+                            const bool fa = pq.x == 1.0; // (1, tan) form, else (cot, 1)
                             if (op.q == 0) {
-                                apply_bit<0, R>(u, v);
-                                if (BWD) { apply_bit<0, R>(u, w); kacc_slot<0, R>(op.b, kk, v, w); }
+                                ry_bit<0, R, BWD>(fa, pq, v);
+                                if (BWD) { ry_bit<0, R, BWD>(fa, pq, w); kacc_slot<0, R>(op.b, kk, v, w); }
                             } else if (R > 1 && op.q == 1) {
-                                apply_bit<(R > 1 ? 1 : 0), R>(u, v);
-                                if (BWD) { apply_bit<(R > 1 ? 1 : 0), R>(u, w); kacc_slot<(R > 1 ? 1 : 0), R>(op.b, kk, v, w); }
+                                ry_bit<(R > 1 ? 1 : 0), R, BWD>(fa, pq, v);
+                                if (BWD) { ry_bit<(R > 1 ? 1 : 0), R, BWD>(fa, pq, w); kacc_slot<(R > 1 ? 1 : 0), R>(op.b, kk, v, w); }
                             } else if (R > 2) {
-                                apply_bit<(R > 2 ? 2 : 0), R>(u, v);
-                                if (BWD) { apply_bit<(R > 2 ? 2 : 0), R>(u, w); kacc_slot<(R > 2 ? 2 : 0), R>(op.b, kk, v, w); }
+                                ry_bit<(R > 2 ? 2 : 0), R, BWD>(fa, pq, v);
+                                if (BWD) { ry_bit<(R > 2 ? 2 : 0), R, BWD>(fa, pq, w); kacc_slot<(R > 2 ? 2 : 0), R>(op.b, kk, v, w); }
                             }
                         } else { // CZ run: Q(x0 | o) = Q(x0) ^ Q(o) ^ parity(o & M(x0))
                             uint32_t qx = 0, M = 0;
@@ -325,6 +401,24 @@ __global__ void __launch_bounds__(kT, 2) seg_c128(const C128Seg sg, const C128Op
                             }
                         }
                     }
+                    if (BWD) {
+#pragma unroll
+                        for (int j = 0; j < NV; ++j) {
+                            const double2 f = cj(tb[j]);
+                            v[j] = cm(f, v[j]);
+                            w[j] = cm(f, w[j]);
+                        }
+#pragma unroll
+                        for (int s2 = 0; s2 < kC128RoundSecs; ++s2) { // Ry scales still applied at K
+                            const double f = kscl[rix * 4 + s2];
+                            kk[s2][0] *= f;
+                            kk[s2][1] *= f;
+                            kk[s2][2] *= f;
+                        }
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < NV; ++j) v[j] = cm(tb[8 + j], v[j]);
+                    }
 #pragma unroll
                     for (int j = 0; j < NV; ++j) {
                         const uint32_t a = slot(j);
@@ -332,17 +426,27 @@ __global__ void __launch_bounds__(kT, 2) seg_c128(const C128Seg sg, const C128Op
                         if (BWD) sl[a] = w[j];
                     }
                 }
-                if (BWD) { // warp sums of the round's (X, Y, Z), added to this warp's slots
+                if (BWD) { // warp sums of the round's (X, Y, Z): one 16-wide reduce-scatter
+                    // (15 shuffles + 1) instead of a butterfly per value (45); lane l < 9 ends
+                    // with value l = 3 slot + component and adds it to this warp's slot
+                    double r[16];
 #pragma unroll
-                    for (uint32_t s2 = 0; s2 < uint32_t(kC128RoundSecs); ++s2) {
-                        if (s2 >= rd.nsec) break;
+                    for (int i = 0; i < 16; ++i) r[i] = i < 9 ? kk[i / 3][i % 3] : 0.0;
 #pragma unroll
-                        for (int c = 0; c < 3; ++c) {
-                            double x = kk[s2][c];
+                    for (int mm = 8; mm >= 1; mm >>= 1) {
+                        const bool up = (lane & uint32_t(mm)) != 0;
 #pragma unroll
-                            for (int o = 16; o >= 1; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-                            if (lane == 0) acc[(rd.sec[s2] * kWarps + warp) * 3 + c] += x;
+                        for (int i = 0; i < mm; ++i) {
+                            const double send = up ? r[i] : r[i + mm];
+                            const double keep = up ? r[i + mm] : r[i];
+                            r[i] = keep + __shfl_xor_sync(0xffffffffu, send, mm);
                         }
+                    }
+                    const double x = r[0] + __shfl_xor_sync(0xffffffffu, r[0], 16);
+                    const uint32_t sl = lane / 3u;
+                    if (lane < 9u && sl < rd.nsec) {
+                        const uint32_t sec = sl == 0 ? rd.sec[0] : sl == 1 ? rd.sec[1] : rd.sec[2];
+                        acc[(sec * kWarps + warp) * 3 + lane % 3u] += x;
                     }
                 }
             }
@@ -504,6 +608,7 @@ C128Plan build_c128_plan(const qf_gate *gates, size_t n_gates, uint32_t n, uint6
                 if (op.type == 0) {
                     const uint32_t p = uint32_t(sg.lpos[opq[o]]);
                     op.q = uint32_t(std::find(bits.begin(), bits.end(), p) - bits.begin());
+                    cur.sbit[op.b] = uint8_t(op.q);
                 } else if (op.type == 1) { // Q of every register offset j
                     uint32_t qo = 0;
                     for (uint32_t jo = 0; jo < (1u << R); ++jo) {
@@ -539,7 +644,9 @@ C128Plan build_c128_plan(const qf_gate *gates, size_t n_gates, uint32_t n, uint6
             if (op.type == 0) {
                 const uint32_t p = uint32_t(sg.lpos[opq[o]]);
                 const bool have = std::find(cur_bits.begin(), cur_bits.end(), p) != cur_bits.end();
-                if (open && (cur.nsec == uint32_t(kC128RoundSecs) || (!have && cur_bits.size() == R))) close();
+                // one section per register bit: the round applies all Rz(g) first and all
+                // Rz(a) last (they commute with everything in the round but their own Ry)
+                if (open && (cur.nsec == uint32_t(kC128RoundSecs) || have || cur_bits.size() == R)) close();
                 if (!open) {
                     cur = C128Round{};
                     cur.op_begin = uint32_t(o);
@@ -600,7 +707,9 @@ cudaError_t launch_c128_segment(cudaStream_t st, bool backward, int grid, const 
                                 double *kpart, unsigned *ticket, double *K) {
     const uint64_t tiles = uint64_t(batch) << sg.nrest;
     const size_t amps = size_t(1) << sg.m;
-    const size_t smax = (size_t(2) << kC128TileBits) * sizeof(double2) + size_t(kC128MaxSec) * kWarps * 3 * sizeof(double);
+    const size_t tabs = size_t(kC128MaxRounds) * (16 * sizeof(double2) + 4 * sizeof(double));
+    const size_t smax = (size_t(2) << kC128TileBits) * sizeof(double2) + tabs +
+                        size_t(kC128MaxSec) * kWarps * 3 * sizeof(double);
     const cudaError_t attr = once_per_device(g_c128_attr, [&] {
         cudaError_t e = cudaSuccess;
 #define QF_C128_ATTR(B, R) \
@@ -612,7 +721,7 @@ cudaError_t launch_c128_segment(cudaStream_t st, bool backward, int grid, const 
     });
     if (attr != cudaSuccess) return attr;
     const int R = int(std::min<uint32_t>(sg.m, 3u));
-    const size_t smem = amps * (backward ? 2 : 1) * sizeof(double2) +
+    const size_t smem = amps * (backward ? 2 : 1) * sizeof(double2) + tabs +
                         (backward ? size_t(std::max<uint32_t>(sg.nsec, 1)) * kWarps * 3 * sizeof(double) : 0);
     if (backward) {
         if (R == 3) launch_seg<true, 3>(st, grid, smem, sg, ops, rounds, cz, secU, psi, lam, n, tiles, kpart, ticket, K);
@@ -627,10 +736,10 @@ cudaError_t launch_c128_segment(cudaStream_t st, bool backward, int grid, const 
 }
 
 cudaError_t launch_c128_finalize(cudaStream_t st, int nsec, const uint32_t *off, const uint32_t *cnt,
-                                 const uint32_t *gates, const double *theta, const double *K,
-                                 double *grad) {
+                                 const uint32_t *gates, const double *theta, const double2 *secU,
+                                 const double *K, double *grad) {
     if (nsec == 0) return cudaSuccess;
-    c128_finalize<<<(nsec + 127) / 128, 128, 0, st>>>(nsec, off, cnt, gates, theta, K, grad);
+    c128_finalize<<<(nsec + 127) / 128, 128, 0, st>>>(nsec, off, cnt, gates, theta, secU, K, grad);
     return cudaGetLastError();
 }
 

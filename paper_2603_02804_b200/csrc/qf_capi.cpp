@@ -937,7 +937,7 @@ void run_c128(qf_ctx *ctx, const qf_gate *gates, size_t n_gates, uint32_t n_qubi
         uint32_t *cz = dupload(F.cz, owned);
         uint32_t *soff = dupload(F.sec_off, owned), *scnt = dupload(F.sec_cnt, owned),
                  *sgat = dupload(F.sec_gates, owned);
-        double2 *secU = dalloc<double2>(size_t(std::max(1, nsec)) * 4, owned);
+        double2 *secU = dalloc<double2>(size_t(std::max(1, nsec)) * kC128SecWords, owned);
         double *K = dalloc<double>(size_t(std::max(1, nsec)) * 8, owned);
         double *kpart = dalloc<double>(size_t(seg_grid) * kC128MaxSec * 8, owned);
         unsigned *ticket = dalloc<unsigned>(1, owned);
@@ -957,7 +957,7 @@ void run_c128(qf_ctx *ctx, const qf_gate *gates, size_t n_gates, uint32_t n_qubi
                "c128 segment");
             st.backward_passes++;
         }
-        ck(launch_c128_finalize(s, nsec, soff, scnt, sgat, th, K, grad_d), "c128 finalize");
+        ck(launch_c128_finalize(s, nsec, soff, scnt, sgat, th, secU, K, grad_d), "c128 finalize");
         ck(launch_reduce_c128(s, nullptr, 0, nullptr, 0, grad_d, epart, chunks, batch, exp_d, loss_d),
            "c128 reduce");
         st.kernel_launches = st.forward_passes + st.backward_passes + 4;

@@ -276,6 +276,7 @@ constexpr int kC128MaxOps = 64;      // ops per segment (staged in shared memory
 constexpr int kC128MaxRounds = 64;   // rounds per segment
 constexpr int kC128MaxCzPairs = 128; // CZ pairs per segment (staged in shared memory)
 constexpr int kC128RoundSecs = 3;    // sections per octet round (K accumulator slots)
+constexpr int kC128SecWords = 8;     // double2 per section in secU (c128_prep)
 struct C128Op {
     uint32_t type; // 0 section, 1 CZ run, 2 CNOT
     uint32_t q;    // section: register bit in its round | CZ run: Q of the round's octet offsets
@@ -291,6 +292,7 @@ struct C128Round {
     uint8_t bits[4];   // octet: local positions of the register bits (ascending)
     uint8_t gq[4];     // ... and their qubits
     uint8_t sec[4];    // section (index within the segment) of K slot s
+    uint8_t sbit[4];   // register bit of K slot s
 };
 struct C128Seg {
     uint32_t m, nrest, op_begin, op_end, sec_begin, nsec, cz_begin, cz_count, round_begin, round_end;
@@ -315,8 +317,8 @@ cudaError_t launch_c128_segment(cudaStream_t st, bool backward, int grid, const 
                                 const double2 *secU, double2 *psi, double2 *lam, int n, uint32_t batch,
                                 double *kpart, unsigned *ticket, double *K);
 cudaError_t launch_c128_finalize(cudaStream_t st, int nsec, const uint32_t *off, const uint32_t *cnt,
-                                 const uint32_t *gates, const double *theta, const double *K,
-                                 double *grad);
+                                 const uint32_t *gates, const double *theta, const double2 *secU,
+                                 const double *K, double *grad);
 
 // cudaFuncSetAttribute opt-ins (e.g. > 48 KiB of dynamic shared memory) are
 // per device: `set` runs once on every device the process launches on (bit d
