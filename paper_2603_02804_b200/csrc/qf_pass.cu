@@ -224,7 +224,7 @@ __global__ void __launch_bounds__(kDualThreads, 1)
     const uint32_t gtid = tid & 255u;
     // light passes (layout B) are bound by the one-tile-deep ring: their next ring
     // load is prefetched into L2 (QF_L2PF=0 disables)
-#ifndef QF_L2PF_NPH
+#ifndef QF_L2PF_NPH // (4-phase programs measured with the prefetch: +0.4% backward time)
 #define QF_L2PF_NPH 3
 #endif
     const bool L2PF = PROG != 0 && prog_nph(PROG) <= QF_L2PF_NPH && p.l2pf;

@@ -740,3 +740,22 @@ def test_balanced_backward_matches_plain(ctx, monkeypatch):
     b = run()
     assert rel_diff(a.gradient, b.gradient) <= 1e-5
     assert rel_diff(a.expect, b.expect) == 0.0  # same forward schedule
+
+
+def test_balanced_backward_ragged_alias_memsave(ctx, oracle):
+    """n = 20 balanced backward on a plan with a ragged batch (3 samples), psi0
+    aliased from caller device memory, MemSave slots, two gradients on the same
+    plan (the second with a new theta)."""
+    import torch
+    n, layers, batch = 20, 6, 3
+    gates, npar, theta, psi0, pauli = _hea_case(n, layers, batch, seed=77)
+    plan = capi.Plan(ctx, gates, n, npar, layers, 2, batch, pauli, storage="memsave")
+    dev = torch.from_numpy(psi0.reshape(-1).copy()).to("cuda")
+    torch.cuda.synchronize()
+    plan.set_psi0_device(dev.data_ptr())
+    for th in (theta, C.random_parameters(npar, 4242)):
+        res = plan.gradient(th)
+        loss, grad, exp = oracle.gradient(gates, n, npar, psi0, th, pauli)
+        assert rel_diff(res.gradient, grad) <= MEMSAVE_TOL
+        assert rel_diff(res.expect, exp) <= TOL  # the final state stays complex64
+    plan.close()
