@@ -199,6 +199,27 @@ int qf_plan_synchronize(qf_plan *plan);
 int qf_plan_traffic(const qf_plan *plan, uint64_t *total_bytes, uint64_t *pass_bytes,
                     uint64_t *passes_per_gradient);
 
+/* Host-only description of the schedule qf_plan_create would build (no device, no
+ * allocation): the planner's decisions, for tests and capacity planning. */
+typedef struct qf_plan_info {
+    uint32_t stages;           /* device stages (HEA: one per layer) */
+    uint32_t resident;         /* 1: sample-resident kernel (n <= 12) */
+    uint32_t layouts;          /* streaming pass layouts (0 when resident) */
+    uint32_t passes;           /* forward passes per gradient (= backward passes) */
+    uint32_t slots;            /* checkpoint slots */
+    uint32_t ckpt_passes;      /* passes per checkpoint block */
+    uint32_t balanced;         /* 1: balanced backward schedule (17 <= n <= 20, even block) */
+    uint32_t wide_forward;     /* forward passes on the 64-amplitude wide kernel */
+    uint32_t compiled_forward; /* forward passes on compiled phase programs (incl. wide) */
+    uint32_t compiled_backward;/* backward passes on compiled phase programs */
+    uint64_t bytes_per_sample; /* algorithmic HBM bytes of one gradient per sample
+                                  (fwd 2S, bwd 4S or 3S after a slot, observable 2S;
+                                  resident: psi0 + slot writes and reads) */
+} qf_plan_info;
+int qf_plan_describe(const qf_gate *gates, size_t n_gates, uint32_t n_qubits, uint32_t n_params,
+                     uint32_t layers, uint32_t ckpt_layers, uint32_t batch, uint64_t x_mask,
+                     uint64_t z_mask, qf_plan_info *out);
+
 /* Synthetic batch store on the device: new_random_state<float>(n, batch, seed)
  * (statevec.cpp:32-53) for samples [first_sample, first_sample + batch) of
  * the global stream, written straight into the plan's psi0 store. */

@@ -27,7 +27,7 @@ SYMBOLS = (
     "qf_gradient_c128",
     "qf_gradient_pergate_c128",
     "qf_plan_create",
-    "qf_plan_create_ex", "qf_plan_destroy",
+    "qf_plan_create_ex", "qf_plan_destroy", "qf_plan_describe",
     "qf_plan_upload_psi0", "qf_plan_set_psi0_device", "qf_plan_gradient",
     "qf_plan_gradient_device", "qf_plan_gradient_pergate", "qf_plan_forward_state",
     "qf_plan_stream", "qf_plan_synchronize", "qf_plan_traffic", "qf_plan_random_psi0", "qf_plan_download_psi0",
@@ -66,6 +66,15 @@ class QfStats(C.Structure):
         ("passes_per_layer", C.c_uint32), ("ckpt_layers", C.c_uint32),
         ("resident", C.c_uint32), ("stages", C.c_uint32), ("device_ms", C.c_double),
     ]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+class QfPlanInfo(C.Structure):
+    _fields_ = [(f, C.c_uint32) for f in (
+        "stages", "resident", "layouts", "passes", "slots", "ckpt_passes", "balanced",
+        "wide_forward", "compiled_forward", "compiled_backward")] + [("bytes_per_sample", C.c_uint64)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -121,6 +130,8 @@ def load(path: str = LIB_PATH):
     L.qf_plan_traffic.argtypes = [_P, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64),
                                   C.POINTER(C.c_uint64)]
     L.qf_plan_random_psi0.argtypes = [_P, C.c_uint64, C.c_uint64]
+    L.qf_plan_describe.argtypes = [_P, C.c_size_t, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
+                                   C.c_uint32, C.c_uint64, C.c_uint64, _P]
     L.qf_plan_download_psi0.argtypes = [_P, _P]
     L.qf_plan_set_profiling.argtypes = [_P, C.c_int]
     L.qf_plan_profile.argtypes = [_P, C.POINTER(QfProfile), C.c_int]
@@ -304,6 +315,16 @@ class Plan:
             self.close()
         except Exception:
             pass
+
+
+def describe_plan(gates, n_qubits, n_params, layers, ckpt_layers, batch, pauli) -> dict:
+    """qf_plan_describe: the schedule qf_plan_create would build (host only, no device)."""
+    load()
+    g = _gates(gates)
+    info = QfPlanInfo()
+    _check(_lib.qf_plan_describe(_ptr(g), len(g), n_qubits, n_params, layers, ckpt_layers, batch,
+                                 pauli[0], pauli[1], C.byref(info)))
+    return info.as_dict()
 
 
 def gradient_c64(ctx: Context, gates, n_qubits, n_params, layers, ckpt_layers, psi0, theta,

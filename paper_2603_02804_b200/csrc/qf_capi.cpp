@@ -1079,6 +1079,48 @@ int qf_plan_create_ex(qf_ctx *ctx, const qf_gate *gates, size_t n_gates, uint32_
     });
 }
 
+int qf_plan_describe(const qf_gate *gates, size_t n_gates, uint32_t n_qubits, uint32_t n_params,
+                     uint32_t layers, uint32_t ckpt_layers, uint32_t batch, uint64_t x_mask,
+                     uint64_t z_mask, qf_plan_info *out) {
+    return guarded([&] {
+        if (!out) throw std::invalid_argument("null output pointer");
+        const Plan P = make_plan(gates, n_gates, n_qubits, n_params, layers, ckpt_layers, batch,
+                                 x_mask, z_mask);
+        qf_plan_info info{};
+        info.stages = P.stages;
+        info.resident = P.resident ? 1u : 0u;
+        info.slots = P.n_slots;
+        const uint64_t S = uint64_t(8) << P.n; // bytes of one sample's state
+        if (P.resident) {
+            info.bytes_per_sample = S * (1 + 2 * uint64_t(P.n_slots));
+        } else {
+            const size_t NPS = P.steps.size();
+            info.layouts = uint32_t(P.layouts.size());
+            info.passes = uint32_t(NPS);
+            info.ckpt_passes = P.ckpt_passes;
+            info.balanced = P.alt ? 1u : 0u;
+            auto prog_of = [&](const PassStep &ps) {
+                const uint32_t rot = (ps.rot0 | ps.rot1) ? (ps.rot0 | ps.rot1) : P.layouts[ps.layout].rot_mask;
+                return prog_encode(ps.nph, ps.ph, rot);
+            };
+            uint64_t units = 2; // observable: read psi, write lambda
+            for (size_t pi = 0; pi < NPS; ++pi) {
+                const PassStep &f = P.steps[pi];
+                const uint32_t pf = prog_of(f);
+                const bool wide = P.wide && f.layout == 0 && f.sd >= 0 && pf == kProgA;
+                info.wide_forward += wide ? 1u : 0u;
+                info.compiled_forward += (wide || prog_compiled(false, pf)) ? 1u : 0u;
+                const PassStep &b = P.bstep(pi);
+                const bool z = b.s0 == 0 || b.s1 == 0; // stage-0 Z measurement: runtime kernel
+                info.compiled_backward += (!z && prog_compiled(true, prog_of(b))) ? 1u : 0u;
+                units += 2 + ((pi > 0 && !P.slot_pass(pi - 1)) ? 4 : 3);
+            }
+            info.bytes_per_sample = S * units;
+        }
+        *out = info;
+    });
+}
+
 int qf_plan_destroy(qf_plan *plan) {
     return guarded([&] { delete plan; });
 }

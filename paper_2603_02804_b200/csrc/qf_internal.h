@@ -202,6 +202,9 @@ int wide_grid(int sms);
 // The forward pass runs the wide kernel (interior layout-A pass with wide tables);
 // its grid is wide_grid(sms) instead of the narrow kernels' occupancy x sms.
 bool pass_is_wide(bool backward, const PassParams &p);
+// A pass with this phase-program code runs a compiled straight-line instance
+// (launch_pass); otherwise the runtime-dispatch kernel.
+bool prog_compiled(bool backward, uint32_t prog);
 cudaError_t launch_pass_wide(cudaStream_t st, int grid, const PassParams &p, const CUtensorMap *psi_in,
                              const CUtensorMap *psi_out);
 cudaError_t launch_pass(cudaStream_t st, bool backward, int grid, const PassParams &p,

@@ -435,6 +435,14 @@ int pass_occupancy(bool backward) {
     return blocks;
 }
 
+bool prog_compiled(bool backward, uint32_t prog) {
+    if (prog == 0 || !progs_enabled()) return false;
+    if (prog == kProgA || prog == kProgB20 || prog == kProgB16 || prog == kProgB16x ||
+        prog == kProgB20P || prog == kProgB16xP)
+        return true;
+    return backward && (prog == kProgAlt || prog == kProgAltP);
+}
+
 bool pass_is_wide(bool backward, const PassParams &p) {
     static const bool enabled = [] {
         const char *e = getenv("QF_WIDE"); // QF_WIDE=0: narrow kernels only (A/B timing)

@@ -80,3 +80,58 @@ def test_python_binding_validates_shapes():
         pkg.capi.gradient_c64(None, gates, 4, npar, 2, 0, good, theta[:-1], pauli)
     with pytest.raises(pkg.capi.QfInvalidArgument):
         pkg.capi.gradient_c128(None, gates, 4, npar, 2, 0, good.astype(np.float64)[:, :5], theta, pauli)
+
+
+# ---- the planner, host only (qf_plan_describe): the schedule decisions of DESIGN.md §3-4
+def _describe(n, layers, k, batch=4):
+    from paper_2603_02804_b200 import capi
+    from paper_2603_02804_b200 import circuits as C
+    gates, npar = C.build_hea(n, layers)
+    return capi.describe_plan(gates, n, npar, layers, k, batch, C.parse_pauli(C.repeated_ixyz_label(n)))
+
+
+def test_plan_hea20q_schedule():
+    """hea20q (config 4's shard): one pass per stage plus the closing pass, the
+    balanced backward with slots after layout-A passes, every interior pass on a
+    compiled program, the wide kernel for the layout-A forwards, and the
+    algorithmic bytes the bench's roofline uses (fwd 2S, bwd 4S / 3S, observable 2S)."""
+    d = _describe(20, 1000, 10, batch=125)
+    assert d["resident"] == 0 and d["layouts"] == 2 and d["stages"] == 1000
+    assert d["passes"] == 1001 and d["ckpt_passes"] == 10 and d["slots"] == 101
+    assert d["balanced"] == 1
+    assert d["wide_forward"] == 499  # interior layout-A passes (not the first, not the last)
+    assert d["compiled_forward"] >= 999 and d["compiled_backward"] >= 998
+    S = 8 << 20
+    # no psi store (3S): the 100 passes right after a slot (psi re-read from the slot)
+    # and the last backward pass (pass 0: nothing reads its psi)
+    no_store = 101
+    assert d["bytes_per_sample"] == S * (2 * 1001 + 4 * (1001 - no_store) + 3 * no_store + 2)
+
+
+def test_plan_balanced_backward_conditions():
+    assert _describe(20, 12, 3)["balanced"] == 0   # odd slot period
+    assert _describe(19, 20, 10)["balanced"] == 1  # partial rows in layout B
+    assert _describe(17, 20, 10)["balanced"] == 1
+    assert _describe(16, 20, 10)["balanced"] == 0  # 13..16: the column group moved to B instead
+    d22 = _describe(22, 4, 2)
+    assert d22["layouts"] == 3 and d22["balanced"] == 0
+
+
+def test_plan_compiled_programs_cover_interior_passes():
+    """13 <= n <= 19 (partial-row layout B) and n = 16: every pass but the first
+    and last runs a compiled straight-line program in both directions."""
+    for n in (13, 14, 15, 16, 17, 18, 19, 20):
+        d = _describe(n, 20, 10)
+        assert d["passes"] == 21, n
+        assert d["compiled_forward"] >= d["passes"] - 2, (n, d)
+        assert d["compiled_backward"] >= d["passes"] - 3, (n, d)  # stage-0 Z passes excluded
+
+
+def test_plan_resident_and_errors():
+    from paper_2603_02804_b200 import capi
+    d = _describe(12, 100, 10, batch=1024)
+    assert d["resident"] == 1 and d["stages"] == 100 and d["slots"] == 9
+    assert d["bytes_per_sample"] == (8 << 12) * (1 + 2 * 9)
+    import pytest
+    with pytest.raises(capi.QfInvalidArgument):
+        _describe(12, 100, 7)  # CheckpointPlan::uniform: 7 does not divide 100
