@@ -572,6 +572,9 @@ void enqueue_fused(qf_plan *pl, const double *theta_dev, double *out_dev, qf_sta
                                     : ms  ? pl->W
                                           : pl->slots + size_t(P.n_slots - 1) * pl->amps_padded;
         auto slot16 = [&](size_t pi) { return pl->slots16 + P.slot_index(pi) * pl->amps_padded; };
+        // layout A's tiles are contiguous runs of 4096 amplitudes (local qubits 0..11)
+        const bool L0_contiguous = !P.layouts.empty() && P.layouts[0].tile_lo_bits == 0 &&
+                                   P.layouts[0].row_start == 4;
         // forward (MemSave: every pass in place on W; a slot pass is narrowed into its bf16 slot)
         std::unique_ptr<Nvtx> range(new Nvtx("qfuse forward"));
         for (size_t pi = 0; pi < NPS; ++pi) {
@@ -583,13 +586,15 @@ void enqueue_fused(qf_plan *pl, const double *theta_dev, double *out_dev, qf_sta
             const CUtensorMap *outm = (!ms && P.slot_pass(pi)) ? &pl->m_slot[P.slot_index(pi)][ps.layout]
                                                                : &pl->m_W[ps.layout];
             PassParams p = pass_params(pl, ps, true);
-            const int grid = pass_is_wide(false, p) ? std::min(wide_grid(pl->ctx->sms), p.tiles)
-                                                    : std::min(pl->grid_fwd, p.tiles);
-            pl->timed(0, 2 * sb, [&] { ck(launch_pass(s, false, grid, p, in, outm, nullptr), "pass fwd"); });
+            const bool wide = pass_is_wide(false, p);
+            const bool narrow = ms && P.slot_pass(pi) && pi + 1 < NPS && !forward_only;
+            if (narrow && wide && ps.layout == 0 && L0_contiguous) p.slot16 = slot16(pi); // fused narrow
+            const int grid = wide ? std::min(wide_grid(pl->ctx->sms), p.tiles) : std::min(pl->grid_fwd, p.tiles);
+            pl->timed(0, (p.slot16 ? 2.5 : 2.0) * sb, [&] { ck(launch_pass(s, false, grid, p, in, outm, nullptr), "pass fwd"); });
             st.kernel_launches++;
             st.forward_passes++;
-            bytes += 2 * sb;
-            if (ms && P.slot_pass(pi) && pi + 1 < NPS && !forward_only) {
+            bytes += (p.slot16 ? 2.5 : 2.0) * sb;
+            if (narrow && !p.slot16) {
                 pl->timed(6, 1.5 * sb, [&] { ck(launch_narrow_bf16(s, pl->W, slot16(pi), pl->amps_padded), "narrow"); });
                 st.kernel_launches++;
                 bytes += 1.5 * sb;

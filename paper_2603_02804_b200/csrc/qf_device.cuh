@@ -360,6 +360,13 @@ __device__ __forceinline__ void kmeasure(const float2 (&p)[16], const float2 (&l
     }
 }
 
+// narrow_to_bf16 (statevec.hpp:36-45): round to nearest even, NaN quieted
+__device__ __forceinline__ uint32_t bf16_rne_bits(float v) {
+    const uint32_t u = __float_as_uint(v);
+    if ((u & 0x7fffffffu) > 0x7f800000u) return (u >> 16) | 0x0040u;
+    return (u + 0x7fffu + ((u >> 16) & 1u)) >> 16;
+}
+
 // ------------------------------------------------------------- diagonal
 __device__ __forceinline__ uint32_t linmask4(uint32_t M) {
     uint32_t m = 0;

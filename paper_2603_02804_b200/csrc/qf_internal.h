@@ -143,6 +143,7 @@ struct PassParams {
     int l2pf;          // backward light passes: L2 prefetch of the next ring load
     double *kpart;     // backward: [grid][stages][n][8]
     long long kstride; // stages*n*8
+    uint32_t *slot16;  // MemSave: the pass also writes its output as bf16 pairs here (wide forward)
 };
 
 // n <= 12: a tile holds 2^(12-n) whole samples; every stage runs in smem.

@@ -242,6 +242,22 @@ __global__ void __launch_bounds__(T * kTeam, 1)
         wsts<1>(pt, tau, v);
         fence_async_smem();
         team_bar(bar_id);
+        if (p.slot16) {
+            // StorageMode::MemSave slot pass: the tile's bf16 copy straight from shared
+            // memory (narrow_to_bf16, statevec.hpp:36-45), instead of a narrow kernel
+            // re-reading the state (layout A: the tile is amplitudes [4096 t, 4096 t + 4096))
+            uint4 *dst = reinterpret_cast<uint4 *>(p.slot16 + size_t(t) * kTileAmps);
+            const uint32_t base = su32(pt);
+#pragma unroll 4
+            for (uint32_t i = 0; i < uint32_t(kTileAmps) / (4 * kTeam); ++i) {
+                const uint32_t q = i * kTeam + tau, l = 4 * q;
+                const float4 a = lds128(base + swz(l)), b = lds128(base + swz(l + 2));
+                dst[q] = make_uint4(bf16_rne_bits(a.x) | (bf16_rne_bits(a.y) << 16),
+                                    bf16_rne_bits(a.z) | (bf16_rne_bits(a.w) << 16),
+                                    bf16_rne_bits(b.x) | (bf16_rne_bits(b.y) << 16),
+                                    bf16_rne_bits(b.z) | (bf16_rne_bits(b.w) << 16));
+            }
+        }
         if (tau == 0) {
             const int c1 = t & lo_mask, c3 = (t >> p.tile_lo_bits) & hi_mask, c4 = t >> sample_shift;
             tma_store5(&m_out, pt, 0, c1, 0, c3, c4);
