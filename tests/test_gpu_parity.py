@@ -399,7 +399,7 @@ def test_config4_depth_fused_vs_pergate(ctx):
 MEMSAVE_TOL = 5e-3  # acceptance.cpp:466-499 (bf16 storage vs fp32)
 
 
-@pytest.mark.parametrize("n,layers,batch,k", [(14, 6, 2, 1), (16, 8, 2, 2), (20, 4, 1, 1)])
+@pytest.mark.parametrize("n,layers,batch,k", [(14, 6, 2, 1), (16, 8, 2, 2), (20, 4, 1, 1), (20, 6, 1, 2), (21, 4, 1, 2)])
 def test_memsave_matches_oracle(ctx, oracle, n, layers, batch, k):
     gates, npar, theta, psi0, pauli = _hea_case(n, layers, batch, seed=900 + n)
     ms = capi.gradient_c64(ctx, gates, n, npar, layers, k, psi0, theta, pauli, storage="memsave")
