@@ -759,3 +759,17 @@ def test_balanced_backward_ragged_alias_memsave(ctx, oracle):
         assert rel_diff(res.gradient, grad) <= MEMSAVE_TOL
         assert rel_diff(res.expect, exp) <= TOL  # the final state stays complex64
     plan.close()
+
+
+def test_balanced_backward_run_to_run_identical(ctx):
+    """Acceptance C11 (acceptance.cpp:501-530) on the 20q balanced schedule: two
+    gradients of the same plan are bit-identical (fixed-order fp64 reductions)."""
+    n, layers, batch = 20, 10, 2
+    gates, npar, theta, psi0, pauli = _hea_case(n, layers, batch, seed=11)
+    plan = capi.Plan(ctx, gates, n, npar, layers, 2, batch, pauli)
+    plan.upload_psi0(psi0)
+    a = plan.gradient(theta)
+    b = plan.gradient(theta)
+    assert np.array_equal(a.gradient, b.gradient) and a.loss == b.loss
+    assert np.array_equal(a.expect, b.expect)
+    plan.close()
